@@ -1,0 +1,407 @@
+// capi.cpp -- the extern "C" boundary (include/so2dr_cuda.h). Converts C
+// structs into engine requests and the library's exception types
+// (include/so2dr/errors.hpp, mirroring proj/include/so2dr/errors.hpp) into
+// so2dr_status codes plus a per-context message.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <stdexcept>
+
+#include "engine.h"
+#include "so2dr/verify.hpp"
+#include "so2dr_cuda.h"
+
+namespace {
+
+thread_local std::string tl_err, tl_constraint, tl_alloc;
+
+so2dr_status fail(so2dr_ctx* ctx, so2dr_status st, const std::string& msg,
+                  const std::string& constraint = "", const std::string& alloc = "") {
+  tl_err = msg;
+  tl_constraint = constraint;
+  tl_alloc = alloc;
+  if (ctx) {
+    ctx->err = msg;
+    ctx->constraint = constraint;
+    ctx->alloc_id = alloc;
+  }
+  return st;
+}
+
+template <typename F>
+so2dr_status guard(so2dr_ctx* ctx, F&& f) {
+  try {
+    f();
+    if (ctx) ctx->err.clear();
+    return SO2DR_OK;
+  } catch (const so2dr::InfeasibleError& e) {
+    return fail(ctx, SO2DR_ERR_INFEASIBLE, e.what(), e.constraint());
+  } catch (const so2dr::OutOfDeviceMemoryError& e) {
+    return fail(ctx, SO2DR_ERR_DEVICE_OOM, e.what(), "", e.allocation_id());
+  } catch (const so2dr::InvalidSpecError& e) {
+    return fail(ctx, SO2DR_ERR_INVALID_SPEC, e.what());
+  } catch (const so2dr::ContractError& e) {
+    return fail(ctx, SO2DR_ERR_CONTRACT, e.what());
+  } catch (const so2dr::IoError& e) {
+    return fail(ctx, SO2DR_ERR_IO, e.what());
+  } catch (const so2dr::DeviceError& e) {
+    return fail(ctx, SO2DR_ERR_CUDA, e.what());
+  } catch (const std::out_of_range& e) {
+    return fail(ctx, SO2DR_ERR_OUT_OF_RANGE, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, SO2DR_ERR_CUDA, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(ctx, SO2DR_ERR_CONTRACT, e.what());
+  }
+}
+
+so2dr::RunConfig to_cfg(const so2dr_run_config* c) {
+  if (!c) throw so2dr::InvalidSpecError("run config is NULL");
+  so2dr::RunConfig r;
+  r.sz = c->sz, r.r = c->r, r.d = c->d, r.s_tb = c->s_tb, r.k_on = c->k_on;
+  r.n_strm = c->n_strm, r.n = c->n, r.n_a = c->n_a;
+  return r;
+}
+
+so2dr::KernelPlan to_kp(const so2dr_kernel_plan* k) {
+  so2dr::KernelPlan p;
+  if (k) {
+    p.k_on = k->k_on;
+    p.tile = k->tile;
+    p.scratch_budget = k->scratch_budget;
+  }
+  return p;
+}
+
+so2dr::HardwareModel to_hw(const so2dr_hardware* h) {
+  so2dr::HardwareModel hw = so2dr::b200_hardware();
+  if (h) {
+    hw.c_dmem = h->c_dmem;
+    hw.bw_dmem = h->bw_dmem;
+    hw.bw_intc = h->bw_intc;
+    hw.b_elem = h->b_elem;
+  }
+  return hw;
+}
+
+void need_ctx(so2dr_ctx* ctx) {
+  if (!ctx) throw so2dr::ContractError("context is NULL");
+}
+
+int dtype_of(so2dr_dtype d) {
+  if (d != SO2DR_F32 && d != SO2DR_F64) throw so2dr::InvalidSpecError("unknown dtype");
+  return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+int so2dr_abi_version(void) { return SO2DR_ABI_VERSION; }
+
+int so2dr_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+so2dr_status so2dr_ctx_create(int device, uint64_t budget_bytes, so2dr_ctx** out) {
+  if (!out) return fail(nullptr, SO2DR_ERR_CONTRACT, "so2dr_ctx_create: out is NULL");
+  *out = nullptr;
+  return guard(nullptr, [&] {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      throw so2dr::DeviceError(
+          "no CUDA device available (the SO2DR engine has no CPU fallback): " +
+          std::string(cudaGetErrorString(e)));
+    }
+    if (device < 0 || device >= n) throw so2dr::InvalidSpecError("device index out of range");
+    SO2DR_CK(cudaSetDevice(device));
+    size_t free_b = 0, total_b = 0;
+    SO2DR_CK(cudaMemGetInfo(&free_b, &total_b));
+    auto* ctx = new so2dr_ctx();
+    ctx->device = device;
+    ctx->pool.budget = budget_bytes ? budget_bytes : static_cast<uint64_t>(free_b * 0.9);
+    *out = ctx;
+  });
+}
+
+void so2dr_ctx_destroy(so2dr_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (void* p : ctx->slab.opened) cudaIpcCloseMemHandle(p);
+  for (auto& kv : ctx->registered) cudaHostUnregister(kv.first);
+  for (cudaStream_t s : ctx->streams) cudaStreamDestroy(s);
+  delete ctx;
+}
+
+so2dr_status so2dr_ctx_set_profiling(so2dr_ctx* ctx, int enable) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    ctx->profiling = enable != 0;
+  });
+}
+
+const char* so2dr_last_error(const so2dr_ctx* ctx) { return ctx ? ctx->err.c_str() : tl_err.c_str(); }
+const char* so2dr_last_constraint(const so2dr_ctx* ctx) {
+  return ctx ? ctx->constraint.c_str() : tl_constraint.c_str();
+}
+const char* so2dr_last_allocation_id(const so2dr_ctx* ctx) {
+  return ctx ? ctx->alloc_id.c_str() : tl_alloc.c_str();
+}
+
+so2dr_status so2dr_host_register(so2dr_ctx* ctx, void* base, size_t bytes) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    if (!base || !bytes) throw so2dr::ContractError("host_register: empty range");
+    if (ctx->registered.count(base)) return;
+    SO2DR_CK(cudaSetDevice(ctx->device));
+    SO2DR_CK(cudaHostRegister(base, bytes, cudaHostRegisterPortable));
+    ctx->registered[base] = bytes;
+  });
+}
+
+so2dr_status so2dr_host_unregister(so2dr_ctx* ctx, void* base) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    auto it = ctx->registered.find(base);
+    if (it == ctx->registered.end()) throw so2dr::ContractError("host_unregister: range not registered");
+    SO2DR_CK(cudaHostUnregister(base));
+    ctx->registered.erase(it);
+  });
+}
+
+so2dr_status so2dr_run(so2dr_ctx* ctx, so2dr_mode mode, const so2dr_stencil_desc* st,
+                       const so2dr_run_config* cfg, const so2dr_kernel_plan* kp,
+                       const so2dr_hardware* hw, const so2dr_hooks* hooks, so2dr_dtype dtype,
+                       void* grid, so2dr_ledger* ledger_out, so2dr_timing* timing_out,
+                       so2dr_diag_row* diag, size_t diag_cap, size_t* n_diag) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    if (mode != SO2DR_MODE_SO2DR && mode != SO2DR_MODE_RESREU && mode != SO2DR_MODE_INCORE)
+      throw so2dr::InvalidSpecError("unknown engine mode");
+    so2dr_eng::RunRequest q;
+    q.mode = mode;
+    q.st = so2dr_eng::make_stencil(st);
+    q.cfg = to_cfg(cfg);
+    q.kp = to_kp(kp);
+    q.hw = to_hw(hw);
+    if (hooks) q.hooks = *hooks;
+    q.dtype = dtype_of(dtype);
+    if (!grid) throw so2dr::ContractError("grid pointer is NULL");
+    q.grid = grid;
+    so2dr_eng::RunResponse out;
+    so2dr_eng::run(ctx, q, out);
+    if (ledger_out) *ledger_out = out.ledger;
+    if (timing_out) *timing_out = out.timing;
+    if (n_diag) *n_diag = out.diag.size();
+    if (diag)
+      std::memcpy(diag, out.diag.data(), std::min(diag_cap, out.diag.size()) * sizeof(so2dr_diag_row));
+  });
+}
+
+so2dr_status so2dr_slab_rows(const so2dr_run_config* cfg, int dim, int rank, int world,
+                             int64_t* lo, int64_t* hi) {
+  return guard(nullptr, [&] {
+    if (!cfg || !lo || !hi) throw so2dr::ContractError("slab_rows: NULL argument");
+    so2dr_eng::slab_rows(*cfg, dim, rank, world, lo, hi);
+  });
+}
+
+so2dr_status so2dr_slab_prepare(so2dr_ctx* ctx, const so2dr_stencil_desc* st,
+                                const so2dr_run_config* cfg, so2dr_dtype dtype, int rank,
+                                int world, uint8_t blob_out[SO2DR_PEER_BLOB_BYTES]) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    if (!cfg || !blob_out) throw so2dr::ContractError("slab_prepare: NULL argument");
+    const so2dr_eng::StencilDev s = so2dr_eng::make_stencil(st);
+    so2dr_eng::slab_prepare(ctx, s, *cfg, dtype_of(dtype), rank, world, blob_out);
+  });
+}
+
+so2dr_status so2dr_slab_connect(so2dr_ctx* ctx, const uint8_t* lower_blob,
+                                const uint8_t* upper_blob) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    so2dr_eng::slab_connect(ctx, lower_blob, upper_blob);
+  });
+}
+
+so2dr_status so2dr_slab_run(so2dr_ctx* ctx, const so2dr_stencil_desc* st,
+                            const so2dr_run_config* cfg, const so2dr_kernel_plan* kp,
+                            so2dr_dtype dtype, void* slab, so2dr_ledger* ledger_out,
+                            so2dr_timing* timing_out) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    const so2dr_eng::SlabState& sl = ctx->slab;
+    if (!sl.prepared) throw so2dr::ContractError("slab_run before slab_prepare");
+    if (!cfg || std::memcmp(cfg, &sl.cfg, sizeof(*cfg)) != 0)
+      throw so2dr::ContractError("slab_run: config differs from the prepared one");
+    if (sl.rank > 0 && !sl.lower.connected) throw so2dr::ContractError("slab_run: not connected");
+    if (sl.rank < sl.world - 1 && !sl.upper.connected)
+      throw so2dr::ContractError("slab_run: not connected");
+    so2dr_eng::RunRequest q;
+    q.mode = SO2DR_MODE_SO2DR;
+    q.st = so2dr_eng::make_stencil(st);
+    q.cfg = to_cfg(cfg);
+    q.kp = to_kp(kp);
+    q.hw = so2dr::b200_hardware();
+    q.hw.c_dmem = ~0ull;
+    q.dtype = dtype_of(dtype);
+    if (q.dtype != sl.dtype || q.st.dim != sl.dim)
+      throw so2dr::ContractError("slab_run: dtype/dim differ from the prepared ones");
+    q.grid = slab;
+    q.rank = sl.rank;
+    q.world = sl.world;
+    int64_t lo, hi;
+    so2dr_eng::slab_rows(*cfg, q.st.dim, sl.rank, sl.world, &lo, &hi);
+    q.host_lo = lo;
+    so2dr_eng::RunResponse out;
+    so2dr_eng::run(ctx, q, out);
+    if (ledger_out) *ledger_out = out.ledger;
+    if (timing_out) *timing_out = out.timing;
+  });
+}
+
+so2dr_status so2dr_fused_kernel(so2dr_ctx* ctx, const so2dr_stencil_desc* st, so2dr_dtype dtype,
+                                void* buf0, void* buf1, int base_row, int rows, int cols,
+                                int read, int steps, int tile, const int32_t region[4],
+                                const int32_t interior[4], const int32_t owned[4],
+                                uint64_t stats_out[4]) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    if (!buf0 || !buf1 || !region || !interior || !owned || !stats_out)
+      throw so2dr::ContractError("fused_kernel: NULL argument");
+    const so2dr_eng::StencilDev s = so2dr_eng::make_stencil(st);
+    so2dr_eng::fused_kernel_host(ctx, s, dtype_of(dtype), buf0, buf1, base_row, rows, cols, read,
+                                 steps, tile, region, interior, owned, stats_out);
+  });
+}
+
+so2dr_status so2dr_apply_step(so2dr_ctx* ctx, const so2dr_stencil_desc* st, so2dr_dtype dtype,
+                              int sz, int r, const void* in, void* out, int row_lo, int row_hi) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    const so2dr_eng::StencilDev s = so2dr_eng::make_stencil(st);
+    if (s.radius != r) throw so2dr::ContractError("apply_step: stencil radius differs from grid ring");
+    so2dr_eng::apply_step_host(ctx, s, dtype_of(dtype), sz, r, in, out, row_lo, row_hi);
+  });
+}
+
+so2dr_status so2dr_run_reference(so2dr_ctx* ctx, const so2dr_stencil_desc* st, so2dr_dtype dtype,
+                                 int sz, int r, const void* in, void* out, int steps) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    const so2dr_eng::StencilDev s = so2dr_eng::make_stencil(st);
+    if (s.radius != r) throw so2dr::ContractError("run_reference: stencil radius differs from grid ring");
+    so2dr_eng::run_reference_host(ctx, s, dtype_of(dtype), sz, r, in, out, steps);
+  });
+}
+
+so2dr_status so2dr_init_grid(so2dr_ctx* ctx, so2dr_dtype dtype, int dim, int sz, int r,
+                             uint64_t seed, void* out) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    so2dr_eng::init_rows(ctx, dtype_of(dtype), dim, sz, r, seed, 0, sz + 2 * r, out);
+  });
+}
+
+so2dr_status so2dr_init_rows(so2dr_ctx* ctx, so2dr_dtype dtype, int dim, int sz, int r,
+                             uint64_t seed, int64_t lo, int64_t hi, void* out) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    so2dr_eng::init_rows(ctx, dtype_of(dtype), dim, sz, r, seed, lo, hi, out);
+  });
+}
+
+uint64_t so2dr_grid_checksum(const void* data, size_t bytes) {
+  const auto* p = static_cast<const unsigned char*>(data);
+  uint64_t h = 0xCBF29CE484222325ULL;
+  for (size_t i = 0; i < bytes; ++i) h = (h ^ p[i]) * 0x100000001B3ULL;
+  return h;
+}
+
+so2dr_status so2dr_kernel_stats(int radius, int steps, int tile, const int32_t region[4],
+                                const int32_t interior[4], const int32_t owned[4], int sy0,
+                                int sy1, int64_t cols, uint64_t stats_out[4]) {
+  return guard(nullptr, [&] {
+    if (!region || !interior || !owned || !stats_out)
+      throw so2dr::ContractError("kernel_stats: NULL argument");
+    if (steps < 1) throw so2dr::InvalidSpecError("fused_kernel: steps must be >= 1");
+    if (tile < 1) throw so2dr::InvalidSpecError("fused_kernel: tile must be >= 1");
+    const so2dr::KernelStats ks = so2dr_eng::tile_stats(
+        radius, steps, tile, so2dr::Rect{region[0], region[1], region[2], region[3]},
+        so2dr::Rect{interior[0], interior[1], interior[2], interior[3]},
+        so2dr::Rect{owned[0], owned[1], owned[2], owned[3]}, sy0, sy1, cols);
+    stats_out[0] = ks.scratch_load;
+    stats_out[1] = ks.scratch_store;
+    stats_out[2] = ks.updates;
+    stats_out[3] = ks.redundant;
+  });
+}
+
+so2dr_status so2dr_arena_bytes(const so2dr_run_config* cfg, const so2dr_kernel_plan* kp,
+                               uint64_t* out) {
+  return guard(nullptr, [&] {
+    if (!out) throw so2dr::ContractError("arena_bytes: out is NULL");
+    *out = so2dr::so2dr_arena_bytes(to_cfg(cfg), to_kp(kp));
+  });
+}
+
+so2dr_status so2dr_device_bytes(const so2dr_run_config* cfg, int dim, so2dr_dtype dtype,
+                                uint64_t* out) {
+  return guard(nullptr, [&] {
+    if (!out) throw so2dr::ContractError("device_bytes: out is NULL");
+    const so2dr::RunConfig c = to_cfg(cfg);
+    c.validate();
+    const so2dr_eng::Geo g = so2dr_eng::make_geo(dim, c.sz, c.r, dtype_of(dtype));
+    *out = so2dr_eng::device_footprint(c, g, c.n_strm);
+  });
+}
+
+so2dr_status so2dr_plan_chunks(const so2dr_run_config* cfg, int32_t* fence_out,
+                               int32_t* chunks_out) {
+  return guard(nullptr, [&] {
+    const so2dr::ChunkLayout L = so2dr::plan_chunks(to_cfg(cfg));
+    if (fence_out)
+      for (size_t i = 0; i < L.fence.size(); ++i) fence_out[i] = L.fence[i];
+    if (chunks_out)
+      for (size_t i = 0; i < L.chunks.size(); ++i) {
+        const so2dr::ChunkIntervals& c = L.chunks[i];
+        const so2dr::RowInterval iv[5] = {c.core, c.working, c.transfer, c.shared_in, c.shared_out};
+        for (int k = 0; k < 5; ++k) {
+          chunks_out[i * 10 + 2 * k] = iv[k].lo;
+          chunks_out[i * 10 + 2 * k + 1] = iv[k].hi;
+        }
+      }
+  });
+}
+
+so2dr_status so2dr_expected_ledger(so2dr_mode mode, const so2dr_run_config* cfg,
+                                   const so2dr_kernel_plan* kp, int dim, so2dr_dtype dtype,
+                                   uint64_t out6[6], int32_t* exact) {
+  return guard(nullptr, [&] {
+    if (!out6) throw so2dr::ContractError("expected_ledger: out is NULL");
+    const so2dr::RunConfig c = to_cfg(cfg);
+    const so2dr::ExpectedLedger e =
+        so2dr::expected_ledger(static_cast<so2dr::EngineMode>(mode), c, to_kp(kp));
+    // the closed forms count 2D fp32 rows; scale to planes / 8-byte cells
+    const uint64_t p = c.padded();
+    const uint64_t scale = (dim == 3 ? p : 1) * (dtype == SO2DR_F64 ? 2 : 1);
+    out6[0] = e.htod * scale;
+    out6[1] = e.dtoh * scale;
+    out6[2] = e.ondevice * scale;
+    out6[3] = e.kernel_invocations;
+    out6[4] = e.rounds;
+    out6[5] = e.redundant_updates * (dim == 3 ? p : 1);
+    if (exact) *exact = e.redundancy_exact ? 1 : 0;
+  });
+}
+
+}  // extern "C"

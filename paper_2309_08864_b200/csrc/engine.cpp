@@ -1,0 +1,981 @@
+// engine.cu -- the B200 SO2DR out-of-core scheduler.
+//
+// Replaces the reference executor proj/src/engine.cpp:200-449
+// (run_out_of_core, so2dr_chunk, resreu_chunk, run_incore). Where the
+// reference runs N_strm std::thread workers that memcpy between host vectors
+// and synchronise through Gates (engine.cpp:75-120), this engine enqueues the
+// whole run from ONE host thread onto N_strm CUDA streams; every
+// happens-before edge of the reference becomes a cudaEvent wait:
+//
+//   stream(i % N_strm):  [wait D2H_{t-1}(i+1)] H2D(transfer_i) -> ring rows ->
+//                        [wait PUB(i-1)] slot -> shared_in, record SLOTFREE ->
+//                        [wait SLOTFREE(slot)] shared_out -> slot, record PUB(i) ->
+//                        K1 x calls_in_round -> D2H(core_i), record D2H(i)
+//
+// The host never blocks until the final synchronize, so H2D, kernels and
+// D2H of different chunks overlap on the two copy engines and the SMs.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+
+#include "engine.h"
+
+namespace so2dr {
+std::string next_share_buffer_id();  // host_model.cpp
+}
+
+namespace so2dr_eng {
+
+using so2dr::ContractError;
+using so2dr::InvalidSpecError;
+using so2dr::OutOfDeviceMemoryError;
+using so2dr::Rect;
+using so2dr::RowInterval;
+
+void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  throw so2dr::DeviceError(std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                           cudaGetErrorString(e) + ") in " + what + " at " + file + ":" +
+                           std::to_string(line));
+}
+
+static void check_cu(CUresult e, const char* what) {
+  if (e == CUDA_SUCCESS) return;
+  throw so2dr::DeviceError(std::string("CUDA driver error ") + std::to_string(static_cast<int>(e)) +
+                           " in " + what);
+}
+
+// Stream memory operations (device-side flag wait/write) come from the driver
+// API; resolve them through the runtime so the library loads (and its host
+// helpers work) on machines without a driver.
+namespace {
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+template <typename Fn>
+Fn driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPointByVersion(name, &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !p)
+    throw so2dr::DeviceError(std::string("driver entry point ") + name + " unavailable");
+  return reinterpret_cast<Fn>(p);
+}
+
+CUresult cuStreamWaitValue32_rt(CUstream s, CUdeviceptr a, cuuint32_t v, unsigned int f) {
+  static WaitFn fn = driver_fn<WaitFn>("cuStreamWaitValue32");
+  return fn(s, a, v, f);
+}
+CUresult cuStreamWriteValue32_rt(CUstream s, CUdeviceptr a, cuuint32_t v, unsigned int f) {
+  static WriteFn fn = driver_fn<WriteFn>("cuStreamWriteValue32");
+  return fn(s, a, v, f);
+}
+}  // namespace
+#undef cuStreamWaitValue32
+#undef cuStreamWriteValue32
+#define cuStreamWaitValue32 cuStreamWaitValue32_rt
+#define cuStreamWriteValue32 cuStreamWriteValue32_rt
+
+// ------------------------------------------------------------------ pools --
+
+void* Pool::get(const std::string& id, uint64_t bytes) {
+  bytes = std::max<uint64_t>(bytes, 256);
+  auto it = blk_.find(id);
+  if (it != blk_.end() && it->second.bytes >= bytes) return it->second.p;
+  const uint64_t others = used() - (it != blk_.end() ? it->second.bytes : 0);
+  if (others + bytes > budget)
+    throw OutOfDeviceMemoryError("hbm:" + id, bytes, others, budget);
+  if (it != blk_.end()) {
+    cudaFree(it->second.p);
+    blk_.erase(it);
+  }
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    throw OutOfDeviceMemoryError("hbm:" + id, bytes, others, budget);
+  }
+  SO2DR_CK(e);
+  blk_[id] = Blk{p, bytes};
+  return p;
+}
+
+uint64_t Pool::used() const {
+  uint64_t u = 0;
+  for (const auto& kv : blk_) u += kv.second.bytes;
+  return u;
+}
+
+void Pool::release_all() {
+  for (auto& kv : blk_) cudaFree(kv.second.p);
+  blk_.clear();
+}
+
+cudaEvent_t EventPool::sync_event() {
+  if (sync_next_ == sync_.size()) {
+    cudaEvent_t e;
+    SO2DR_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    sync_.push_back(e);
+  }
+  return sync_[sync_next_++];
+}
+
+cudaEvent_t EventPool::timing_event() {
+  if (timing_next_ == timing_.size()) {
+    cudaEvent_t e;
+    SO2DR_CK(cudaEventCreate(&e));
+    timing_.push_back(e);
+  }
+  return timing_[timing_next_++];
+}
+
+void EventPool::recycle() { sync_next_ = timing_next_ = 0; }
+
+EventPool::~EventPool() {
+  for (auto e : sync_) cudaEventDestroy(e);
+  for (auto e : timing_) cudaEventDestroy(e);
+}
+
+}  // namespace so2dr_eng
+
+cudaStream_t so2dr_ctx::stream(int i) {
+  while (static_cast<int>(streams.size()) <= i) {
+    cudaStream_t s;
+    SO2DR_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    streams.push_back(s);
+  }
+  return streams[i];
+}
+
+namespace so2dr_eng {
+
+// --------------------------------------------------------------- geometry --
+
+Geo make_geo(int dim, int sz, int r, int dtype) {
+  Geo g;
+  g.dim = dim;
+  g.sz = sz;
+  g.r = r;
+  g.p = sz + 2 * r;
+  g.elem = dtype == SO2DR_F64 ? 8 : 4;
+  g.pitch = (static_cast<int64_t>(g.p) + 31) / 32 * 32;
+  g.unit_rows = dim == 3 ? g.p : 1;
+  return g;
+}
+
+StencilDev make_stencil(const so2dr_stencil_desc* st) {
+  if (!st) throw InvalidSpecError("stencil descriptor is NULL");
+  StencilDev s;
+  s.dim = st->dim;
+  s.radius = st->radius;
+  if (s.dim != 2 && s.dim != 3) throw InvalidSpecError("stencil dim must be 2 or 3");
+  if (st->kind == SO2DR_KIND_GRADIENT) {
+    if (s.dim != 2) throw InvalidSpecError("gradient stencil is 2D only");
+    if (s.radius != 1) throw InvalidSpecError("gradient stencil has radius 1");
+    s.kind = so2dr_dev::KGRAD;
+    s.w.assign(9, 0.0);
+    return s;
+  }
+  if (st->kind != SO2DR_KIND_BOX && st->kind != SO2DR_KIND_STAR)
+    throw InvalidSpecError("unknown stencil kind " + std::to_string(st->kind));
+  const int rmax = s.dim == 2 ? 4 : 2;
+  if (s.radius < 1 || s.radius > rmax)
+    throw InvalidSpecError("stencil radius must be in 1.." + std::to_string(rmax) + " for dim " +
+                           std::to_string(s.dim));
+  const int e = 2 * s.radius + 1;
+  const int n = s.dim == 3 ? e * e * e : e * e;
+  if (!st->weights) throw InvalidSpecError("stencil weights are NULL");
+  s.w.assign(st->weights, st->weights + n);
+  bool off_axis_zero = true;
+  for (int i = 0; i < n; ++i) {
+    if (!std::isfinite(s.w[i])) throw InvalidSpecError("tap weight not finite");
+    const int dx = i % e - s.radius, dy = (i / e) % e - s.radius;
+    const int dz = s.dim == 3 ? i / (e * e) - s.radius : 0;
+    const int axes = (dz != 0) + (dy != 0) + (dx != 0);
+    if (axes > 1 && s.w[i] != 0.0) off_axis_zero = false;
+  }
+  // A box whose off-axis weights are all zero runs on the star kernel: the
+  // skipped taps are fma(0, v, acc) == acc for finite v (acc never -0).
+  s.kind = (st->kind == SO2DR_KIND_STAR || off_axis_zero) ? so2dr_dev::KSTAR : so2dr_dev::KBOX;
+  if (s.kind == so2dr_dev::KSTAR)
+    for (int i = 0; i < n; ++i) {
+      const int dx = i % e - s.radius, dy = (i / e) % e - s.radius;
+      const int dz = s.dim == 3 ? i / (e * e) - s.radius : 0;
+      if ((dz != 0) + (dy != 0) + (dx != 0) > 1) s.w[i] = 0.0;
+    }
+  return s;
+}
+
+// --------------------------------------------------- ledger (closed form) --
+// Sum over tiles [a_t, b_t) covering [A, B) with edge T of
+// max(0, min(b_t + e, hi) - max(a_t - e, lo)).
+static uint64_t tile_span_sum(int64_t A, int64_t B, int64_t T, int64_t e, int64_t lo, int64_t hi,
+                              bool exhaustive) {
+  if (B <= A) return 0;
+  const int64_t nt = (B - A + T - 1) / T;
+  if (exhaustive || nt <= 64) {
+    uint64_t s = 0;
+    for (int64_t t = 0; t < nt; ++t) {
+      const int64_t a = A + t * T, b = std::min(a + T, B);
+      const int64_t v = std::min(b + e, hi) - std::max(a - e, lo);
+      if (v > 0) s += static_cast<uint64_t>(v);
+    }
+    return s;
+  }
+  // every tile is positive here (columns are never clipped to the interior):
+  // sum of (width + 2e) minus the clipping at both storage edges.
+  int64_t s = (B - A) + 2 * e * nt;
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t a = A + t * T;
+    if (a - e >= lo) break;
+    s -= lo - (a - e);
+  }
+  for (int64_t t = nt - 1; t >= 0; --t) {
+    const int64_t b = std::min(A + (t + 1) * T, B);
+    if (b + e <= hi) break;
+    s -= (b + e) - hi;
+  }
+  return static_cast<uint64_t>(s);
+}
+
+// proj/src/kernels.cpp:48-138: scratch load/store, element updates (all columns
+// of interior rows) and redundant updates of one fused_kernel call for tile T.
+so2dr::KernelStats tile_stats(int r, int steps, int tile, Rect region, Rect interior, Rect owned,
+                              int sy0, int sy1, int64_t cols) {
+  so2dr::KernelStats ks;
+  if (region.area() == 0) return ks;
+  const int64_t e0 = static_cast<int64_t>(r) * steps;
+  const uint64_t ly = tile_span_sum(region.y0, region.y1, tile, e0, sy0, sy1, true);
+  const uint64_t lx = tile_span_sum(region.x0, region.x1, tile, e0, 0, cols, false);
+  uint64_t updates = 0, owned_total = 0;
+  for (int u = 1; u <= steps; ++u) {
+    const int64_t e = static_cast<int64_t>(r) * (steps - u);
+    // rows: clip to storage, then count only interior rows
+    const int64_t ilo = std::max<int64_t>(sy0, interior.y0), ihi = std::min<int64_t>(sy1, interior.y1);
+    uint64_t ky = 0;
+    if (ihi > ilo) {
+      const int64_t nt = (region.height() + tile - 1) / tile;
+      for (int64_t t = 0; t < nt; ++t) {
+        const int64_t a = region.y0 + t * tile, b = std::min<int64_t>(a + tile, region.y1);
+        const int64_t cy0 = std::max<int64_t>(a - e, sy0), cy1 = std::min<int64_t>(b + e, sy1);
+        const int64_t v = std::min(cy1, ihi) - std::max(cy0, ilo);
+        if (v > 0) ky += static_cast<uint64_t>(v);
+      }
+    }
+    const uint64_t cx = tile_span_sum(region.x0, region.x1, tile, e, 0, cols, false);
+    updates += ky * cx;
+    const int64_t uy0 = std::max<int64_t>({region.y0 - e, interior.y0, sy0});
+    const int64_t uy1 = std::min<int64_t>({region.y1 + e, interior.y1, sy1});
+    const int64_t ux0 = std::max<int64_t>(region.x0 - e, 0), ux1 = std::min<int64_t>(region.x1 + e, cols);
+    const int64_t ry0 = std::max<int64_t>(uy0, owned.y0), ry1 = std::min<int64_t>(uy1, owned.y1);
+    const int64_t rx0 = std::max<int64_t>(ux0, owned.x0), rx1 = std::min<int64_t>(ux1, owned.x1);
+    if (ry1 > ry0 && rx1 > rx0) owned_total += static_cast<uint64_t>((ry1 - ry0) * (rx1 - rx0));
+  }
+  ks.scratch_load = ly * lx * sizeof(float);
+  ks.scratch_store = region.area() * sizeof(float);
+  ks.updates = updates;
+  ks.redundant = updates - std::min(owned_total, updates);
+  return ks;
+}
+
+// ----------------------------------------------------------- K1 dispatch --
+
+void k1_call(so2dr_ctx* ctx, cudaStream_t s, const Geo& g, const StencilDev& st, const void* rd,
+             void* wr, int base, int rows, int y0, int y1, int x0, int x1, int steps,
+             int scratch_slot, const int32_t* interior) {
+  if (y1 <= y0 || x1 <= x0 || steps < 1) return;
+  so2dr_dev::K1Launch L;
+  L.dim = g.dim;
+  L.dtype = g.elem == 8 ? 1 : 0;
+  L.kind = st.kind;
+  L.radius = st.radius;
+  L.pitch = g.pitch;
+  L.base = base;
+  L.rows = rows;
+  L.cols = g.dim == 3 ? g.p : g.p;
+  L.plane_rows = g.dim == 3 ? g.p : 0;
+  L.iy0 = interior ? interior[0] : g.r;
+  L.iy1 = interior ? interior[1] : g.r + g.sz;
+  L.ix0 = interior ? interior[2] : g.r;
+  L.ix1 = interior ? interior[3] : g.p - g.r;
+  L.w = st.w.data();
+  const int m = so2dr_dev::k1_max_steps(g.dim, L.dtype, st.kind, st.radius);
+  if (m < 1) throw InvalidSpecError("no K1 kernel for this stencil shape");
+  // Kernel contract (see k1_2d.cuh): every row/column an interior update of
+  // the trapezoid reads must be in storage. Reads reach region +- r*steps but
+  // never beyond the interior +- r (cells outside the interior pass through),
+  // so storage may be clipped only across the ring.
+  const int R = st.radius;
+  const int need_lo = std::max(y0 - R * steps, L.iy0 - R);
+  const int need_hi = std::min(y1 + R * steps, L.iy1 + R);
+  if (need_lo < base || need_hi > base + rows)
+    throw ContractError("fused kernel: region needs rows [" + std::to_string(need_lo) + "," +
+                        std::to_string(need_hi) + ") outside field storage [" +
+                        std::to_string(base) + "," + std::to_string(base + rows) + ")");
+  const int ncols = L.cols;
+  if (std::max(x0 - R * steps, L.ix0 - R) < 0 || std::min(x1 + R * steps, L.ix1 + R) > ncols)
+    throw ContractError("fused kernel: region needs columns outside the field");
+  auto launch = [&](const void* in, void* out, int ly0, int ly1, int lx0, int lx1, int sub) {
+    L.in = in;
+    L.out = out;
+    L.steps = sub;
+    L.y0 = ly0;
+    L.y1 = ly1;
+    L.x0 = lx0;
+    L.x1 = lx1;
+    SO2DR_CK(so2dr_dev::k1_launch(L, s));
+  };
+  if (steps <= m) {
+    launch(rd, wr, y0, y1, x0, x1, steps);
+    return;
+  }
+  // Split into ceil(steps/m) launches. Intermediate launches produce the
+  // trapezoid rows still needed (region grown by r*remaining steps) into two
+  // scratch fields; only the last launch writes the destination, so cells of
+  // `wr` outside the region stay untouched (reference semantics).
+  const uint64_t field_bytes = static_cast<uint64_t>(rows) * g.dev_unit_elems() * g.elem;
+  void* scr[2] = {ctx->pool.get("scratch" + std::to_string(scratch_slot) + ".a", field_bytes),
+                  ctx->pool.get("scratch" + std::to_string(scratch_slot) + ".b", field_bytes)};
+  const int pieces = (steps + m - 1) / m;
+  int remaining = steps;
+  const void* in = rd;
+  for (int k = 0; k < pieces; ++k) {
+    const int sub = (k == 0) ? steps - m * (pieces - 1) : m;
+    remaining -= sub;
+    const int grow = R * remaining;
+    const int ly0 = std::max(base, y0 - grow), ly1 = std::min(base + rows, y1 + grow);
+    const int lx0 = std::max(0, x0 - grow), lx1 = std::min(g.dim == 3 ? g.p : g.p, x1 + grow);
+    void* out = (k == pieces - 1) ? wr : scr[k & 1];
+    launch(in, out, ly0, ly1, lx0, lx1, sub);
+    in = out;
+  }
+}
+
+uint64_t device_footprint(const so2dr::RunConfig& cfg, const Geo& g, int n_strm) {
+  const int h = cfg.r * cfg.s_tb;
+  const int core = cfg.sz / cfg.d;
+  const uint64_t work_units = std::min<uint64_t>(core + 2 * h + cfg.r, g.top());
+  const uint64_t unit = static_cast<uint64_t>(g.dev_unit_elems()) * g.elem;
+  const uint64_t slots = static_cast<uint64_t>(std::max(2, n_strm)) * 2 * h * unit;
+  return 2ull * n_strm * work_units * unit + slots;
+}
+
+// -------------------------------------------------------- copy utilities --
+
+// Copy `n` units between a device field (pitch g.pitch) and the grid (host or
+// device, dense rows of g.p cells). Uses the 2D copy engine path.
+static void copy_units(const Geo& g, void* dst, int64_t dst_pitch, const void* src,
+                       int64_t src_pitch, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  SO2DR_CK(cudaMemcpy2DAsync(dst, dst_pitch * g.elem, src, src_pitch * g.elem,
+                             static_cast<size_t>(g.p) * g.elem,
+                             static_cast<size_t>(n * g.unit_rows), cudaMemcpyDefault, s));
+}
+
+struct Field {
+  char* buf[2] = {nullptr, nullptr};
+  int base = 0;  // unit index of storage row 0
+};
+
+struct RunCtx {
+  so2dr_ctx* ctx;
+  const Geo& g;
+  char* host;       // grid pointer == unit host_lo
+  int64_t host_lo;
+  RunResponse& out;
+  bool profile;
+
+  char* dev_at(const Field& f, int which, int unit) const {
+    return f.buf[which] + static_cast<int64_t>(unit - f.base) * g.dev_unit_elems() * g.elem;
+  }
+  char* host_at(int unit) const {
+    return host + (static_cast<int64_t>(unit) - host_lo) * g.host_unit_elems() * g.elem;
+  }
+  void h2d(const Field& f, int which, RowInterval rows, cudaStream_t s) const {
+    copy_units(g, dev_at(f, which, rows.lo), g.pitch, host_at(rows.lo), g.p, rows.height(), s);
+  }
+  void d2h(const Field& f, int which, RowInterval rows, cudaStream_t s) const {
+    copy_units(g, host_at(rows.lo), g.p, dev_at(f, which, rows.lo), g.pitch, rows.height(), s);
+  }
+  void d2d(char* dst, const char* src, int64_t units, cudaStream_t s) const {
+    if (units <= 0) return;
+    SO2DR_CK(cudaMemcpyAsync(dst, src, static_cast<size_t>(units * g.dev_unit_elems() * g.elem),
+                             cudaMemcpyDeviceToDevice, s));
+  }
+  uint64_t bytes(int64_t units) const { return static_cast<uint64_t>(units) * g.unit_bytes(); }
+
+  // timed region helpers
+  cudaEvent_t stage_begin(cudaStream_t s) const {
+    if (!profile) return nullptr;
+    cudaEvent_t e = ctx->events.timing_event();
+    SO2DR_CK(cudaEventRecord(e, s));
+    return e;
+  }
+  void stage_end(cudaEvent_t b, cudaStream_t s, int round, int chunk, so2dr::Stage st,
+                 uint64_t bytes, uint64_t updates,
+                 std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& pend,
+                 std::vector<size_t>& pend_idx) const {
+    so2dr_diag_row row{};
+    row.round = round;
+    row.chunk = chunk;
+    row.stage = static_cast<int>(st);
+    row.bytes = bytes;
+    row.updates = updates;
+    out.diag.push_back(row);
+    if (profile && b) {
+      cudaEvent_t e = ctx->events.timing_event();
+      SO2DR_CK(cudaEventRecord(e, s));
+      pend.push_back({b, e});
+      pend_idx.push_back(out.diag.size() - 1);
+    }
+  }
+};
+
+// Ledger accumulation (host integers) -------------------------------------
+struct Acc {
+  so2dr_ledger L{};
+  void add_kernel(const so2dr::KernelStats& ks) {
+    L.scratch_load += ks.scratch_load;
+    L.scratch_store += ks.scratch_store;
+    L.element_updates += ks.updates;
+    L.redundant_updates += ks.redundant;
+    L.kernel_invocations += 1;
+  }
+};
+
+// Modeled arena replay (reference allocation sequence, engine.cpp:204-226 and
+// 413-418) against hw.c_dmem; throws OutOfDeviceMemoryError naming the id.
+// Units are rows (2D) or planes (3D); b is the element size, so for 2D fp32 the
+// figures are exactly the reference's.
+static void replay_arena(const RunRequest& q, const so2dr::RunConfig& cfg, const Geo& g,
+                         so2dr_timing& t) {
+  so2dr::DeviceArena arena(q.hw.c_dmem);
+  const uint64_t b = static_cast<uint64_t>(g.elem);
+  const uint64_t unit = static_cast<uint64_t>(g.host_unit_elems());
+  if (q.mode == SO2DR_MODE_INCORE) {
+    const uint64_t gb = static_cast<uint64_t>(g.p) * unit * b;
+    arena.alloc("grid_a", gb);
+    arena.alloc("grid_b", gb);
+    arena.alloc("stream0.scratch", q.kp.scratch_footprint(cfg.r, q.kp.k_on));
+  } else {
+    const so2dr::ChunkLayout lay = so2dr::plan_chunks(cfg);
+    if (q.mode == SO2DR_MODE_SO2DR) {
+      const uint64_t work =
+          (static_cast<uint64_t>(cfg.sz / cfg.d) * unit + 2ull * cfg.r * unit * cfg.s_tb) * b;
+      for (int k = 0; k < cfg.n_strm; ++k) arena.alloc("stream" + std::to_string(k) + ".work", work);
+      const std::string sid = so2dr::next_share_buffer_id();
+      arena.alloc(sid, static_cast<uint64_t>(std::max(2, cfg.n_strm)) * (2ull * cfg.r * cfg.s_tb) *
+                           unit * b);
+    } else {
+      int max_rows = 0;
+      for (int i = 0; i < cfg.d; ++i) {
+        const int hi = i == cfg.d - 1 ? g.p : lay.fence[i + 1];
+        const int lo = i == 0 ? 0 : lay.fence[i] - cfg.r * cfg.s_tb - cfg.r;
+        max_rows = std::max(max_rows, hi - lo);
+      }
+      const uint64_t work = static_cast<uint64_t>(max_rows) * unit * b;
+      for (int k = 0; k < cfg.n_strm; ++k) arena.alloc("stream" + std::to_string(k) + ".work", work);
+      const std::string sid = so2dr::next_share_buffer_id();
+      arena.alloc(sid, static_cast<uint64_t>(cfg.d - 1) * cfg.s_tb * 2ull * cfg.r * unit * b);
+    }
+    for (int k = 0; k < cfg.n_strm; ++k)
+      arena.alloc("stream" + std::to_string(k) + ".scratch",
+                  q.kp.scratch_footprint(cfg.r, q.kp.k_on));
+  }
+  t.arena_peak = arena.peak();
+  t.arena_capacity = arena.capacity();
+}
+
+void validate_request(const RunRequest& q) {
+  q.hw.validate();
+  const so2dr::RunConfig& c = q.cfg;
+  c.validate();
+  q.kp.validate(q.st.radius);
+  if (q.st.radius != c.r) throw ContractError("engine: stencil radius does not match run config");
+}
+
+
+// ------------------------------------------------------------- the modes --
+
+namespace {
+
+using so2dr::Stage;
+
+struct Recorder {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kernel;  // one pair per K1 call
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage;
+  std::vector<size_t> stage_idx;
+  uint64_t alg_bytes = 0;
+};
+
+// One K1 call over rows [y0, y1) x all columns, bracketed by timing events on
+// its own stream (the bench's per-launch kernel time).
+void k1_timed(RunCtx& rc, Recorder& rec, cudaStream_t s, const StencilDev& st, const Field& f,
+              int rows, int rd, int y0, int y1, int steps, int slot) {
+  cudaEvent_t a = rc.ctx->events.timing_event(), b = rc.ctx->events.timing_event();
+  SO2DR_CK(cudaEventRecord(a, s));
+  k1_call(rc.ctx, s, rc.g, st, f.buf[rd], f.buf[rd ^ 1], f.base, rows, y0, y1, 0, rc.g.p, steps,
+          slot, nullptr);
+  SO2DR_CK(cudaEventRecord(b, s));
+  rec.kernel.push_back({a, b});
+  const int lo = std::max(f.base, y0 - st.radius * steps);
+  const int hi = std::min(f.base + rows, y1 + st.radius * steps);
+  rec.alg_bytes += static_cast<uint64_t>((hi - lo) + (y1 - y0)) * rc.g.unit_bytes();
+}
+
+cudaEvent_t record_sync(so2dr_ctx* ctx, cudaStream_t s) {
+  cudaEvent_t e = ctx->events.sync_event();
+  SO2DR_CK(cudaEventRecord(e, s));
+  return e;
+}
+
+void wait(cudaStream_t s, cudaEvent_t e) {
+  if (e) SO2DR_CK(cudaStreamWaitEvent(s, e, 0));
+}
+
+CUdeviceptr dptr(const void* p) { return reinterpret_cast<CUdeviceptr>(p); }
+
+// ---- so2dr: round-based streaming with region sharing (engine.cpp:200-318)
+void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc& acc,
+               Recorder& rec) {
+  so2dr_ctx* ctx = rc.ctx;
+  const Geo& g = rc.g;
+  const so2dr::ChunkLayout lay = so2dr::plan_chunks(cfg);
+  const so2dr::RoundPlan rp = so2dr::make_round_plan(cfg);
+  const int d = cfg.d, ns = cfg.n_strm, r = cfg.r, h = cfg.r * cfg.s_tb;
+  const int slots = std::max(2, ns);
+  const int world = q.world, rank = q.rank;
+  const int dl = d / world;
+  const int cb = rank * dl, ce = cb + dl;  // chunks owned by this rank
+  const bool has_lo = rank > 0, has_hi = rank < world - 1;
+  const Rect interior{r, r + cfg.sz, 0, 0};
+  const int64_t cols = g.host_unit_elems();
+  Rect inter = interior;
+  inter.x0 = g.dim == 3 ? 0 : r;
+  inter.x1 = g.dim == 3 ? static_cast<int>(cols) : g.p - r;
+
+  int max_work = 0;
+  for (int i = cb; i < ce; ++i) max_work = std::max(max_work, lay.chunks[i].working.height());
+  const uint64_t unit = static_cast<uint64_t>(g.dev_unit_elems()) * g.elem;
+  std::vector<Field> F(ns);
+  for (int k = 0; k < ns; ++k)
+    for (int b = 0; b < 2; ++b)
+      F[k].buf[b] = static_cast<char*>(ctx->pool.get(
+          "stream" + std::to_string(k) + ".buf" + std::to_string(b), max_work * unit));
+  std::vector<char*> slot(slots, nullptr);
+  if (dl > 1)
+    for (int j = 0; j < slots; ++j)
+      slot[j] = static_cast<char*>(ctx->pool.get("slot" + std::to_string(j), 2ull * h * unit));
+
+  SlabState& sl = ctx->slab;
+  char* band_lo = nullptr;
+  char* band_hi = nullptr;
+  if (has_lo) band_lo = static_cast<char*>(ctx->pool.get("band.lo", h * unit));
+  if (has_hi) band_hi = static_cast<char*>(ctx->pool.get("band.hi", h * unit));
+  cudaStream_t aux_lo = ctx->stream(ns), aux_hi = ctx->stream(ns + 1);
+
+  std::vector<cudaEvent_t> ev_pub(d, nullptr), ev_d2h(d, nullptr), ev_free(slots, nullptr);
+  cudaEvent_t ev_band_lo = nullptr, ev_band_hi = nullptr, ev_lo_used = nullptr,
+              ev_hi_used = nullptr;
+
+  for (int t = 0; t < rp.rounds; ++t) {
+    const int k_eff = rp.steps_in_round(t);
+    const int calls = rp.calls_in_round(t);
+    const uint32_t epoch = static_cast<uint32_t>(sl.epoch);
+
+    // ---- slab edges: stage our edge bands once, push them to the neighbours
+    if (has_lo) {
+      const RowInterval band{lay.fence[cb], lay.fence[cb] + h};
+      wait(aux_lo, ev_d2h[cb]);
+      wait(aux_lo, ev_lo_used);
+      copy_units(g, band_lo, g.pitch, rc.host_at(band.lo), g.p, h, aux_lo);
+      acc.L.htod += rc.bytes(h);
+      ev_band_lo = record_sync(ctx, aux_lo);
+      check_cu(cuStreamWaitValue32(aux_lo, dptr(&sl.flags[2]), epoch, CU_STREAM_WAIT_VALUE_GEQ),
+               "wait ack lo");
+      SO2DR_CK(cudaMemcpyAsync(sl.lower.recv, band_lo, h * unit, cudaMemcpyDefault, aux_lo));
+      check_cu(cuStreamWriteValue32(aux_lo, dptr(sl.lower.flag), epoch + 1, 0), "signal lo");
+      rc.out.timing.peer_bytes += h * unit;
+    }
+    if (has_hi) {
+      const RowInterval band{lay.fence[ce] - h, lay.fence[ce]};
+      wait(aux_hi, ev_d2h[ce - 1]);
+      wait(aux_hi, ev_hi_used);
+      copy_units(g, band_hi, g.pitch, rc.host_at(band.lo), g.p, h, aux_hi);
+      acc.L.htod += rc.bytes(h);
+      ev_band_hi = record_sync(ctx, aux_hi);
+      check_cu(cuStreamWaitValue32(aux_hi, dptr(&sl.flags[3]), epoch, CU_STREAM_WAIT_VALUE_GEQ),
+               "wait ack hi");
+      SO2DR_CK(cudaMemcpyAsync(sl.upper.recv, band_hi, h * unit, cudaMemcpyDefault, aux_hi));
+      check_cu(cuStreamWriteValue32(aux_hi, dptr(sl.upper.flag), epoch + 1, 0), "signal hi");
+      rc.out.timing.peer_bytes += h * unit;
+    }
+
+    for (int i = cb; i < ce; ++i) {
+      const so2dr::ChunkIntervals& ci = lay.chunks[i];
+      const int sidx = (i - cb) % ns;
+      cudaStream_t s = ctx->stream(sidx);
+      Field& f = F[sidx];
+      f.base = ci.working.lo;
+
+      // host write-after-read across rounds: our transfer rows overlap the
+      // core of chunk i+1, which that chunk wrote back last round
+      if (t > 0 && i + 1 < ce && (i + 1 - cb) % ns != sidx) wait(s, ev_d2h[i + 1]);
+
+      // H2D of the transfer rows (the slab edge bands are already staged)
+      RowInterval tr = ci.transfer;
+      if (i == cb && has_lo) tr.lo = std::max(tr.lo, lay.fence[cb] + h);
+      if (i == ce - 1 && has_hi) tr.hi = lay.fence[ce] - h;
+      cudaEvent_t sb = rc.stage_begin(s);
+      rc.h2d(f, 0, tr, s);
+      acc.L.htod += rc.bytes(tr.height());
+      uint64_t htod_b = rc.bytes(tr.height());
+      // constant ring rows seed the second buffer (engine.cpp:398-401)
+      if (i == 0) rc.d2d(rc.dev_at(f, 1, 0), rc.dev_at(f, 0, 0), r, s);
+      if (i == d - 1) rc.d2d(rc.dev_at(f, 1, r + cfg.sz), rc.dev_at(f, 0, r + cfg.sz), r, s);
+      if (i == ce - 1 && has_hi) {
+        // our upper edge band, then the neighbour's rows above it
+        wait(s, ev_band_hi);
+        rc.d2d(rc.dev_at(f, 0, lay.fence[ce] - h), band_hi, h, s);
+        ev_hi_used = record_sync(ctx, s);
+        check_cu(cuStreamWaitValue32(s, dptr(&sl.flags[1]), epoch + 1, CU_STREAM_WAIT_VALUE_GEQ),
+                 "wait data hi");
+        rc.d2d(rc.dev_at(f, 0, lay.fence[ce]), static_cast<char*>(sl.recv_hi), h, s);
+        check_cu(cuStreamWriteValue32(s, dptr(sl.upper.ack), epoch + 1, 0), "ack hi");
+      }
+      rc.stage_end(sb, s, t, i, Stage::htod, htod_b, 0, rec.stage, rec.stage_idx);
+
+      // region sharing: consume the slab of boundary i-1 (engine.cpp:277-284)
+      if (i > cb) {
+        sb = rc.stage_begin(s);
+        wait(s, ev_pub[i - 1]);
+        const int j = (i - 1) % slots;
+        rc.d2d(rc.dev_at(f, 0, ci.shared_in.lo), slot[j], 2 * h, s);
+        ev_free[j] = record_sync(ctx, s);
+        acc.L.ondevice += rc.bytes(2 * h);
+        rc.stage_end(sb, s, t, i, Stage::share_read, rc.bytes(2 * h), 0, rec.stage,
+                     rec.stage_idx);
+      } else if (has_lo) {
+        sb = rc.stage_begin(s);
+        check_cu(cuStreamWaitValue32(s, dptr(&sl.flags[0]), epoch + 1, CU_STREAM_WAIT_VALUE_GEQ),
+                 "wait data lo");
+        rc.d2d(rc.dev_at(f, 0, lay.fence[cb] - h), static_cast<char*>(sl.recv_lo), h, s);
+        check_cu(cuStreamWriteValue32(s, dptr(sl.lower.ack), epoch + 1, 0), "ack lo");
+        wait(s, ev_band_lo);
+        rc.d2d(rc.dev_at(f, 0, lay.fence[cb]), band_lo, h, s);
+        ev_lo_used = record_sync(ctx, s);
+        rc.stage_end(sb, s, t, i, Stage::share_read, rc.bytes(2 * h), 0, rec.stage,
+                     rec.stage_idx);
+      }
+      // publish the slab of boundary i before any kernel rewrites buf0
+      // (engine.cpp:285-293; SURVEY 7 hard part 5)
+      if (i < ce - 1) {
+        sb = rc.stage_begin(s);
+        const int j = i % slots;
+        wait(s, ev_free[j]);
+        if (q.hooks.corrupt_share && q.hooks.boundary == i)
+          SO2DR_CK(cudaMemsetAsync(slot[j], 0, 2ull * h * unit, s));
+        else
+          rc.d2d(slot[j], rc.dev_at(f, 0, ci.shared_out.lo), 2 * h, s);
+        ev_pub[i] = record_sync(ctx, s);
+        acc.L.ondevice += rc.bytes(2 * h);
+        rc.stage_end(sb, s, t, i, Stage::share_write, rc.bytes(2 * h), 0, rec.stage,
+                     rec.stage_idx);
+      }
+
+      // K1 calls over shrinking trapezoids (engine.cpp:295-310)
+      sb = rc.stage_begin(s);
+      int rd = 0, done = 0;
+      uint64_t kb = 0, ku = 0;
+      for (int c = 0; c < calls; ++c) {
+        const int sc = rp.steps_in_call(t, c);
+        done += sc;
+        const RowInterval area = so2dr::compute_area(lay, i, done, k_eff);
+        k1_timed(rc, rec, s, q.st, f, ci.working.height(), rd, area.lo, area.hi, sc, sidx);
+        const so2dr::KernelStats ks = tile_stats(
+            r, sc, q.kp.tile, Rect{area.lo, area.hi, 0, static_cast<int>(cols)}, inter,
+            Rect{ci.core.lo, ci.core.hi, 0, static_cast<int>(cols)}, ci.working.lo,
+            ci.working.hi, cols);
+        acc.add_kernel(ks);
+        kb += ks.scratch_load + ks.scratch_store;
+        ku += ks.updates;
+        rd ^= 1;
+      }
+      rc.stage_end(sb, s, t, i, Stage::kernel, kb, ku, rec.stage, rec.stage_idx);
+
+      // D2H of the core rows (engine.cpp:312-317)
+      sb = rc.stage_begin(s);
+      rc.d2h(f, rd, ci.core, s);
+      ev_d2h[i] = record_sync(ctx, s);
+      acc.L.dtoh += rc.bytes(ci.core.height());
+      rc.stage_end(sb, s, t, i, Stage::dtoh, rc.bytes(ci.core.height()), 0, rec.stage,
+                   rec.stage_idx);
+    }
+    acc.L.rounds += 1;
+    sl.epoch += 1;
+  }
+}
+
+// ---- incore: whole grid resident, fused kernels (engine.cpp:413-449)
+void run_incore(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc& acc,
+                Recorder& rec) {
+  so2dr_ctx* ctx = rc.ctx;
+  const Geo& g = rc.g;
+  const int r = cfg.r, p = g.p;
+  const uint64_t unit = static_cast<uint64_t>(g.dev_unit_elems()) * g.elem;
+  Field f;
+  f.base = 0;
+  f.buf[0] = static_cast<char*>(ctx->pool.get("stream0.buf0", p * unit));
+  f.buf[1] = static_cast<char*>(ctx->pool.get("stream0.buf1", p * unit));
+  cudaStream_t s = ctx->stream(0);
+  const int64_t cols = g.host_unit_elems();
+  const Rect inter{r, r + cfg.sz, g.dim == 3 ? 0 : r, g.dim == 3 ? static_cast<int>(cols) : p - r};
+
+  cudaEvent_t sb = rc.stage_begin(s);
+  rc.h2d(f, 0, {0, p}, s);
+  acc.L.htod += rc.bytes(p);
+  rc.stage_end(sb, s, 0, 0, Stage::htod, rc.bytes(p), 0, rec.stage, rec.stage_idx);
+  rc.d2d(rc.dev_at(f, 1, 0), rc.dev_at(f, 0, 0), r, s);
+  rc.d2d(rc.dev_at(f, 1, r + cfg.sz), rc.dev_at(f, 0, r + cfg.sz), r, s);
+
+  sb = rc.stage_begin(s);
+  int rd = 0, done = 0;
+  uint64_t kb = 0, ku = 0;
+  const Rect region{r, r + cfg.sz, 0, static_cast<int>(cols)};
+  while (done < cfg.n) {
+    const int sc = std::min(q.kp.k_on, cfg.n - done);
+    k1_timed(rc, rec, s, q.st, f, p, rd, r, r + cfg.sz, sc, 0);
+    const so2dr::KernelStats ks = tile_stats(r, sc, q.kp.tile, region, inter, region, 0, p, cols);
+    acc.add_kernel(ks);
+    kb += ks.scratch_load + ks.scratch_store;
+    ku += ks.updates;
+    rd ^= 1;
+    done += sc;
+  }
+  rc.stage_end(sb, s, 0, 0, Stage::kernel, kb, ku, rec.stage, rec.stage_idx);
+
+  sb = rc.stage_begin(s);
+  rc.d2h(f, rd, {r, r + cfg.sz}, s);
+  acc.L.dtoh += rc.bytes(cfg.sz);
+  rc.stage_end(sb, s, 0, 0, Stage::dtoh, rc.bytes(cfg.sz), 0, rec.stage, rec.stage_idx);
+  acc.L.rounds += 1;
+}
+
+// ---- resreu: skewed ownership, single-step kernels, per-state 2r-row
+// exchange (engine.cpp:321-394)
+void run_resreu(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc& acc,
+                Recorder& rec) {
+  so2dr_ctx* ctx = rc.ctx;
+  const Geo& g = rc.g;
+  const so2dr::ChunkLayout lay = so2dr::plan_chunks(cfg);
+  const so2dr::RoundPlan rp = so2dr::make_round_plan(cfg);
+  const int d = cfg.d, ns = cfg.n_strm, r = cfg.r, p = g.p;
+  const int64_t cols = g.host_unit_elems();
+  const Rect inter{r, r + cfg.sz, g.dim == 3 ? 0 : r, g.dim == 3 ? static_cast<int>(cols) : p - r};
+  auto part = [&](int i) {
+    return RowInterval{i == 0 ? 0 : lay.fence[i], i == d - 1 ? p : lay.fence[i + 1]};
+  };
+  auto extent = [&](int i) {
+    return RowInterval{i == 0 ? 0 : lay.fence[i] - r * cfg.s_tb - r, part(i).hi};
+  };
+  auto skew = [&](int i, int t) {
+    return RowInterval{i == 0 ? r : lay.fence[i] - r * t,
+                       i == d - 1 ? r + cfg.sz : lay.fence[i + 1] - r * t};
+  };
+  int max_rows = 0;
+  for (int i = 0; i < d; ++i) max_rows = std::max(max_rows, extent(i).height());
+  const uint64_t unit = static_cast<uint64_t>(g.dev_unit_elems()) * g.elem;
+  std::vector<Field> F(ns);
+  for (int k = 0; k < ns; ++k)
+    for (int b = 0; b < 2; ++b)
+      F[k].buf[b] = static_cast<char*>(ctx->pool.get(
+          "stream" + std::to_string(k) + ".buf" + std::to_string(b), max_rows * unit));
+  const uint64_t state_bytes = 2ull * r * unit;
+  char* states = d > 1 ? static_cast<char*>(ctx->pool.get(
+                             "states", static_cast<uint64_t>(d - 1) * cfg.s_tb * state_bytes))
+                       : nullptr;
+  auto state_at = [&](int b, int t) { return states + (static_cast<uint64_t>(b) * cfg.s_tb + t) * state_bytes; };
+  std::vector<cudaEvent_t> ev_d2h(d, nullptr);
+  std::vector<cudaEvent_t> ev_state(static_cast<size_t>(std::max(d - 1, 0)) * cfg.s_tb, nullptr);
+
+  for (int t0 = 0; t0 < rp.rounds; ++t0) {
+    const int k_eff = rp.steps_in_round(t0);
+    for (int i = 0; i < d; ++i) {
+      const int sidx = i % ns;
+      cudaStream_t s = ctx->stream(sidx);
+      Field& f = F[sidx];
+      const RowInterval ext = extent(i), pr = part(i);
+      f.base = ext.lo;
+      if (t0 > 0 && i + 1 < d && (i + 1) % ns != sidx) wait(s, ev_d2h[i + 1]);
+      cudaEvent_t sb = rc.stage_begin(s);
+      rc.h2d(f, 0, pr, s);
+      acc.L.htod += rc.bytes(pr.height());
+      rc.stage_end(sb, s, t0, i, Stage::htod, rc.bytes(pr.height()), 0, rec.stage, rec.stage_idx);
+      if (i == 0) rc.d2d(rc.dev_at(f, 1, 0), rc.dev_at(f, 0, 0), r, s);
+      if (i == d - 1) rc.d2d(rc.dev_at(f, 1, r + cfg.sz), rc.dev_at(f, 0, r + cfg.sz), r, s);
+
+      uint64_t share_w = 0, share_r = 0, kb = 0, ku = 0;
+      auto publish = [&](int state, const char* src) {
+        char* dst = state_at(i, state);
+        if (q.hooks.corrupt_share && q.hooks.boundary == i)
+          SO2DR_CK(cudaMemsetAsync(dst, 0, state_bytes, s));
+        else
+          rc.d2d(dst, src, 2 * r, s);
+        ev_state[static_cast<size_t>(i) * cfg.s_tb + state] = record_sync(ctx, s);
+        acc.L.ondevice += rc.bytes(2 * r);
+        share_w += rc.bytes(2 * r);
+      };
+      if (i < d - 1) publish(0, rc.dev_at(f, 0, lay.fence[i + 1] - 2 * r));
+      int rd = 0;
+      for (int t = 1; t <= k_eff; ++t) {
+        if (i > 0) {
+          wait(s, ev_state[static_cast<size_t>(i - 1) * cfg.s_tb + (t - 1)]);
+          rc.d2d(rc.dev_at(f, rd, lay.fence[i] - r * (t - 1) - 2 * r), state_at(i - 1, t - 1),
+                 2 * r, s);
+          acc.L.ondevice += rc.bytes(2 * r);
+          share_r += rc.bytes(2 * r);
+        }
+        const RowInterval rows = skew(i, t);
+        k1_timed(rc, rec, s, q.st, f, ext.height(), rd, rows.lo, rows.hi, 1, sidx);
+        const Rect reg{rows.lo, rows.hi, 0, static_cast<int>(cols)};
+        const so2dr::KernelStats ks = tile_stats(r, 1, q.kp.tile, reg, inter, reg, ext.lo, ext.hi, cols);
+        acc.add_kernel(ks);
+        kb += ks.scratch_load + ks.scratch_store;
+        ku += ks.updates;
+        if (i < d - 1 && t < k_eff) publish(t, rc.dev_at(f, rd ^ 1, lay.fence[i + 1] - r * t - 2 * r));
+        rd ^= 1;
+      }
+      if (share_r) rc.stage_end(nullptr, s, t0, i, Stage::share_read, share_r, 0, rec.stage, rec.stage_idx);
+      if (share_w) rc.stage_end(nullptr, s, t0, i, Stage::share_write, share_w, 0, rec.stage, rec.stage_idx);
+      rc.stage_end(nullptr, s, t0, i, Stage::kernel, kb, ku, rec.stage, rec.stage_idx);
+      const RowInterval owned = skew(i, k_eff);
+      sb = rc.stage_begin(s);
+      rc.d2h(f, rd, owned, s);
+      ev_d2h[i] = record_sync(ctx, s);
+      acc.L.dtoh += rc.bytes(owned.height());
+      rc.stage_end(sb, s, t0, i, Stage::dtoh, rc.bytes(owned.height()), 0, rec.stage, rec.stage_idx);
+    }
+    acc.L.rounds += 1;
+  }
+}
+
+struct HostPin {
+  void* base = nullptr;
+  bool mine = false;
+  ~HostPin() {
+    if (mine) cudaHostUnregister(base);
+  }
+};
+
+}  // namespace
+
+void run(so2dr_ctx* ctx, RunRequest& q, RunResponse& out) {
+  const auto t0 = std::chrono::steady_clock::now();
+  validate_request(q);
+  so2dr::RunConfig cfg = q.cfg;
+  if (q.mode == SO2DR_MODE_RESREU) {
+    cfg.k_on = 1;
+    q.kp.k_on = 1;
+  }
+  if (q.mode == SO2DR_MODE_INCORE) cfg.d = 1;
+  cfg.validate();
+  q.kp.validate(q.st.radius);
+  if (q.world < 1 || q.rank < 0 || q.rank >= q.world) throw InvalidSpecError("bad rank/world");
+  if (q.world > 1) {
+    if (q.mode != SO2DR_MODE_SO2DR) throw InvalidSpecError("slab partitioning runs so2dr mode only");
+    if (cfg.d % q.world != 0)
+      throw InvalidSpecError("config: d (" + std::to_string(cfg.d) +
+                             ") must be divisible by the number of ranks (" +
+                             std::to_string(q.world) + ")");
+  }
+  const Geo g = make_geo(q.st.dim, cfg.sz, cfg.r, q.dtype);
+  replay_arena(q, cfg, g, out.timing);
+  if (q.mode != SO2DR_MODE_INCORE) so2dr::plan_chunks(cfg);  // InfeasibleError before any work
+
+  SO2DR_CK(cudaSetDevice(ctx->device));
+  ctx->events.recycle();
+  out.diag.clear();
+
+  // host grid: pin it for the duration of the call if it is large pageable memory
+  HostPin pin;
+  {
+    cudaPointerAttributes attr{};
+    const cudaError_t e = cudaPointerGetAttributes(&attr, q.grid);
+    if (e != cudaSuccess) cudaGetLastError();
+    int64_t units = g.top();
+    if (q.world > 1) {
+      int64_t lo, hi;
+      slab_rows({cfg.sz, cfg.r, cfg.d, cfg.s_tb, cfg.k_on, cfg.n_strm, cfg.n, cfg.n_a}, g.dim,
+                q.rank, q.world, &lo, &hi);
+      units = hi - lo;
+    }
+    const size_t bytes = static_cast<size_t>(units) * g.host_unit_elems() * g.elem;
+    if (e == cudaSuccess && attr.type == cudaMemoryTypeUnregistered && bytes >= (32u << 20) &&
+        cfg.n > 0) {
+      if (cudaHostRegister(q.grid, bytes, cudaHostRegisterDefault) == cudaSuccess) {
+        pin.base = q.grid;
+        pin.mine = true;
+      } else {
+        cudaGetLastError();
+      }
+    }
+  }
+
+  const int ns = cfg.n_strm;
+  RunCtx rc{ctx, g, static_cast<char*>(q.grid), q.host_lo, out, ctx->profiling};
+  Acc acc;
+  Recorder rec;
+  cudaStream_t s0 = ctx->stream(0);
+  for (int k = 1; k < ns + 2; ++k) ctx->stream(k);
+  cudaEvent_t ev_start = ctx->events.timing_event(), ev_end = ctx->events.timing_event();
+  SO2DR_CK(cudaEventRecord(ev_start, s0));
+  for (int k = 1; k < ns + 2; ++k) wait(ctx->stream(k), ev_start);
+
+  switch (q.mode) {
+    case SO2DR_MODE_SO2DR: run_so2dr(rc, q, cfg, acc, rec); break;
+    case SO2DR_MODE_INCORE: run_incore(rc, q, cfg, acc, rec); break;
+    case SO2DR_MODE_RESREU: run_resreu(rc, q, cfg, acc, rec); break;
+  }
+  for (int k = 1; k < ns + 2; ++k) wait(s0, record_sync(ctx, ctx->stream(k)));
+  SO2DR_CK(cudaEventRecord(ev_end, s0));
+  SO2DR_CK(cudaEventSynchronize(ev_end));
+  SO2DR_CK(cudaGetLastError());
+
+  float ms = 0.f;
+  SO2DR_CK(cudaEventElapsedTime(&ms, ev_start, ev_end));
+  so2dr_timing& tm = out.timing;
+  tm.device_ms = ms;
+  for (const auto& kv : rec.kernel) {
+    float k = 0.f;
+    SO2DR_CK(cudaEventElapsedTime(&k, kv.first, kv.second));
+    tm.kernel_ms += k;
+    tm.kernel_max_ms = std::max<double>(tm.kernel_max_ms, k);
+  }
+  tm.kernel_launches = rec.kernel.size();
+  tm.kernel_alg_bytes = rec.alg_bytes;
+  for (size_t i = 0; i < rec.stage.size(); ++i) {
+    float k = 0.f;
+    SO2DR_CK(cudaEventElapsedTime(&k, rec.stage[i].first, rec.stage[i].second));
+    out.diag[rec.stage_idx[i]].ms = k;
+  }
+  tm.h2d_bytes = acc.L.htod;
+  tm.d2h_bytes = acc.L.dtoh;
+  tm.d2d_bytes = acc.L.ondevice;
+  uint64_t cells = 1;
+  for (int k = 0; k < g.dim; ++k) cells *= static_cast<uint64_t>(cfg.sz);
+  tm.cell_updates = cells * static_cast<uint64_t>(cfg.n) / static_cast<uint64_t>(q.world);
+  tm.device_bytes = ctx->pool.used();
+  out.ledger = acc.L;
+  if (out.ledger.redundant_updates > out.ledger.element_updates)
+    throw ContractError("ledger audit: redundant_updates exceeds element_updates");
+  tm.wall_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace so2dr_eng

@@ -1,0 +1,366 @@
+// k1_2d.cuh -- K1: the k-step temporal-blocked 2D stencil kernel for sm_100a.
+//
+// Replaces the reference's fused_kernel (proj/src/kernels.cpp:27-145) and its
+// per-row arithmetic stencil_row (proj/src/stencil.cpp:120-144).
+//
+// Contract (identical to one reference fused_kernel call): given the read
+// buffer holding rows [base, base+rows) of the padded grid, write into the
+// write buffer the state after S steps of every cell in `region`
+// (rows [y0,y1) x cols [x0,x1)). Cells outside `interior` pass through.
+// Per-point arithmetic is the reference's canonical chain (box: +0 then one
+// FMA per tap in (dy, dx) ascending order; star: the same chain over on-axis
+// taps; gradient: the pinned expression), so results are bit-identical.
+//
+// Design (AN5D-style streaming, B200-first):
+//  * A CTA owns a column strip of NT*V cells (V consecutive cells per thread)
+//    and a segment of output rows; it streams the input rows of the segment
+//    (plus R*S warm-up rows each side) from HBM exactly once. Only the x halo
+//    (R*S columns each side) is recomputed -- the deliberate redundancy of
+//    temporal blocking -- about 2RS/(NT*V) extra work.
+//  * The S time steps are S pipeline stages inside the CTA. Stage u consumes
+//    one row of stage u-1 per iteration and keeps 2R+1 partial accumulators
+//    (one per output row the consumed row contributes to). Because rows arrive
+//    in ascending order, every output point receives its taps in exactly the
+//    canonical (dy, dx) order, so the partial accumulation is bit-exact.
+//  * x neighbours come from warp shuffles; only the two warp-edge lanes go
+//    through shared memory. One __syncthreads per iteration (edge buffers are
+//    double-buffered by iteration parity; each stage consumes what the
+//    previous stage emitted one iteration earlier).
+//  * Input rows are prefetched D rows ahead with 16-byte cp.async (LDGSTS)
+//    into a per-thread shared-memory ring; output rows leave with 16-byte
+//    stores. Each input row is read from HBM once and each output row is
+//    written once: 2*b bytes per cell per launch, i.e. 2b/S per update.
+//  * The main loop is unrolled by 2R+1 so accumulator slot rotation is static
+//    (no local-memory indexing).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <utility>
+
+#include "k1_launch.h"
+
+namespace so2dr_dev {
+
+template <typename T>
+struct K1Args2D {
+  const T* in;      // read buffer; storage row 0 == padded row `base`
+  T* out;           // write buffer, same geometry
+  int64_t pitch;    // elements per storage row (multiple of 32)
+  int base, rows;   // storage rows [base, base+rows)
+  int cols;         // padded width
+  int y0, y1, x0, x1;
+  int iy0, iy1, ix0, ix1;
+  int seg;          // output rows per CTA (y segment)
+  int strip;        // output columns per CTA
+  int xorg;         // thread-column origin of CTA 0 (aligned to VEC)
+  T w[81];          // (2R+1)^2 weights, canonical order
+};
+
+template <typename T>
+__device__ __forceinline__ T fma_rn(T a, T b, T c);
+template <>
+__device__ __forceinline__ float fma_rn<float>(float a, float b, float c) {
+  return __fmaf_rn(a, b, c);
+}
+template <>
+__device__ __forceinline__ double fma_rn<double>(double a, double b, double c) {
+  return __fma_rn(a, b, c);
+}
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <typename T, int V>
+struct VecIO;
+template <>
+struct VecIO<float, 4> {
+  static __device__ __forceinline__ void store(float* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <>
+struct VecIO<double, 2> {
+  static __device__ __forceinline__ void store(double* p, const double (&v)[2]) {
+    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  }
+};
+template <>
+struct VecIO<double, 4> {
+  static __device__ __forceinline__ void store(double* p, const double (&v)[4]) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+  }
+};
+
+// Pipeline depth of the cp.async input ring.
+constexpr int kRing = 4;
+
+template <typename T, int R, int S, int KIND, int V, int NT>
+struct K1Plan2D {
+  static constexpr int E = 2 * R + 1;
+  static constexpr int H = R * S;
+  static constexpr int NW = NT / 32;
+  static constexpr int VEC = 16 / (int)sizeof(T);
+  static_assert(V % VEC == 0, "V must be a whole number of 16-byte vectors");
+  static_assert(R <= V, "warp-shuffle halo needs R <= V");
+  static constexpr int NACC = (KIND == KGRAD) ? 0 : S;
+  static constexpr int NGR = (KIND == KGRAD) ? S : 0;
+};
+
+template <typename T, int R, int S, int KIND, int V, int NT>
+__global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
+  using P = K1Plan2D<T, R, S, KIND, V, NT>;
+  constexpr int E = P::E, H = P::H, NW = P::NW, VEC = P::VEC;
+
+  __shared__ __align__(16) T ring[kRing][NT * V];
+  // warp-edge halo values: [parity][producer stage][warp + 1][side][R]
+  __shared__ T edge[2][S][NW + 2][2][R];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- CTA geometry -------------------------------------------------------
+  const int tc0 = a.xorg + blockIdx.x * a.strip;  // column of thread 0 cell 0
+  const int OX0 = max(tc0 + H, a.x0);
+  const int OX1 = min(tc0 + H + a.strip, a.x1);
+  const int OY0 = a.y0 + blockIdx.y * a.seg;
+  const int OY1 = min(OY0 + a.seg, a.y1);
+  const int sy0 = a.base, sy1 = a.base + a.rows;
+  const int lo0 = max(OY0 - H, sy0), hi0 = min(OY1 + H, sy1);
+  const int n_iter = OY1 - lo0 + S * (R + 1);
+  const int xt = tc0 + tid * V;  // this thread's first column
+
+  // rows produced by each stage: [lo_u, hi_u)
+  int lo[S + 1], hi[S + 1];
+#pragma unroll
+  for (int u = 0; u <= S; ++u) {
+    lo[u] = max(OY0 - R * (S - u), sy0);
+    hi[u] = min(OY1 + R * (S - u), sy1);
+  }
+
+  // columns needing pass-through (ring / outside the grid)
+  unsigned ringmask = 0;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int x = xt + k;
+    if (x < a.ix0 || x >= a.ix1) ringmask |= 1u << k;
+  }
+  // whole 16-byte vectors inside [0, pitch) are loaded (a thread may straddle
+  // column 0 when V > VEC, e.g. fp64 with V=4)
+  const bool load_ok = xt + V > 0 && xt < a.pitch;
+  bool store_full = true, store_any = false;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int x = xt + k;
+    const bool ok = x >= OX0 && x < OX1;
+    store_full = store_full && ok;
+    store_any = store_any || ok;
+  }
+
+  // zero the edge buffers so out-of-strip halo reads are finite garbage
+  for (int i = tid; i < 2 * S * (NW + 2) * 2 * R; i += NT) (&edge[0][0][0][0][0])[i] = T(0);
+
+  T wt[E * E];
+#pragma unroll
+  for (int i = 0; i < E * E; ++i) wt[i] = a.w[i];
+
+  // carried state
+  T cur[S][V];                                   // stage 0..S-1 emitted row (own cells)
+  T acc[P::NACC > 0 ? P::NACC : 1][E][V];        // box/star partial accumulators
+  T grow[P::NGR > 0 ? P::NGR : 1][3][V + 2];     // gradient row window (with x halo)
+#pragma unroll
+  for (int u = 0; u < S; ++u)
+#pragma unroll
+    for (int k = 0; k < V; ++k) cur[u][k] = T(0);
+
+  // ---- prefetch prologue --------------------------------------------------
+  auto issue = [&](int row, int slot) {
+    if (row >= lo0 && row < hi0 && load_ok) {
+      const T* src = a.in + (int64_t)(row - sy0) * a.pitch + xt;
+#pragma unroll
+      for (int v = 0; v < V; v += VEC)
+        if (xt + v >= 0) cp_async16(&ring[slot][tid * V + v], src + v);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int d = 0; d < kRing - 1; ++d) issue(lo0 + d, d);
+  __syncthreads();
+
+  const T* __restrict__ gin = a.in;
+  T* __restrict__ gout = a.out;
+
+  // pass-through value of cell (row, xt+k) from the read buffer
+  auto passthru = [&](int row, int k) -> T {
+    const int x = xt + k;
+    if (x < 0 || x >= a.cols) return T(0);
+    return __ldg(gin + (int64_t)(row - sy0) * a.pitch + x);
+  };
+
+  // One pipeline iteration at compile-time phase PH = it mod E.
+  auto body = [&](auto phase_tag, int it) {
+    constexpr int PH = decltype(phase_tag)::value;
+    const int par = it & 1, ppar = par ^ 1;
+
+    // stages in descending order: stage u consumes cur[u-1] (emitted by stage
+    // u-1 in the previous iteration) before stage u-1 overwrites it.
+#pragma unroll
+    for (int u = S; u >= 1; --u) {
+      const int A = it + lo0 - u - (u - 1) * R;  // row consumed by stage u
+      const int Erow = A - R;                    // row emitted by stage u
+      const bool consume = A >= lo[u - 1] && A < hi[u - 1];
+      const bool emit = Erow >= lo[u] && Erow < hi[u];
+      if (!consume && !emit) continue;
+
+      T seg[V + 2 * R];
+      if (consume) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) seg[R + k] = cur[u - 1][k];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          T l = __shfl_up_sync(0xffffffffu, cur[u - 1][V - R + j], 1);
+          T rr = __shfl_down_sync(0xffffffffu, cur[u - 1][j], 1);
+          if (lane == 0) l = edge[ppar][u - 1][warp][1][j];
+          if (lane == 31) rr = edge[ppar][u - 1][warp + 2][0][j];
+          seg[j] = l;
+          seg[R + V + j] = rr;
+        }
+      }
+
+      T outv[V];
+      if constexpr (KIND == KGRAD) {
+        // rows: slot PH = A (just consumed), PH-1 = A-1 (centre), PH-2 = A-2 (north)
+        constexpr int sA = PH % 3, sC = (PH + 2) % 3, sN = (PH + 1) % 3;
+        if (consume) {
+#pragma unroll
+          for (int k = 0; k < V + 2; ++k) grow[u - 1][sA][k] = seg[k];
+        }
+        if (emit) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            const T c = grow[u - 1][sC][k + 1];
+            const T dn = sub_rn(grow[u - 1][sN][k + 1], c);
+            const T ds = sub_rn(grow[u - 1][sA][k + 1], c);
+            const T de = sub_rn(grow[u - 1][sC][k + 2], c);
+            const T dw = sub_rn(grow[u - 1][sC][k], c);
+            const T sum = add_rn(add_rn(add_rn(dn, ds), de), dw);
+            outv[k] = add_rn(c, mul_rn(T(0.25), sum));
+          }
+        }
+      } else {
+        if (consume) {
+#pragma unroll
+          for (int m = 0; m < E; ++m) {
+            const int dy = m - R;                    // A contributes at dy to row A-dy
+            const int sl = (PH - m + 2 * E) % E;     // slot of output row A+R-m
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+              T x = (m == 0) ? T(0) : acc[u - 1][sl][k];
+              if constexpr (KIND == KBOX) {
+#pragma unroll
+                for (int dx = -R; dx <= R; ++dx)
+                  x = fma_rn(wt[(dy + R) * E + dx + R], seg[R + k + dx], x);
+              } else {  // star: on-axis taps only
+                if (dy != 0) {
+                  x = fma_rn(wt[(dy + R) * E + R], seg[R + k], x);
+                } else {
+#pragma unroll
+                  for (int dx = -R; dx <= R; ++dx)
+                    x = fma_rn(wt[R * E + dx + R], seg[R + k + dx], x);
+                }
+              }
+              acc[u - 1][sl][k] = x;
+            }
+          }
+        }
+        if (emit) {
+          constexpr int se = (PH - 2 * R + 2 * E) % E;  // slot of row A-R
+#pragma unroll
+          for (int k = 0; k < V; ++k) outv[k] = acc[u - 1][se][k];
+        }
+      }
+
+      if (emit) {
+        if (Erow < a.iy0 || Erow >= a.iy1) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) outv[k] = passthru(Erow, k);
+        } else if (ringmask) {
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            if (ringmask & (1u << k)) outv[k] = passthru(Erow, k);
+        }
+        if (u == S) {
+          T* dst = gout + (int64_t)(Erow - sy0) * a.pitch + xt;
+          if (store_full) {
+            VecIO<T, V>::store(dst, outv);
+          } else if (store_any) {
+#pragma unroll
+            for (int k = 0; k < V; ++k)
+              if (xt + k >= OX0 && xt + k < OX1) dst[k] = outv[k];
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < V; ++k) cur[u][k] = outv[k];
+          if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) edge[par][u][warp + 1][0][j] = outv[j];
+          }
+          if (lane == 31) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) edge[par][u][warp + 1][1][j] = outv[V - R + j];
+          }
+        }
+      }
+    }
+
+    // stage 0: row lo0 + it arrives from the cp.async ring
+    {
+      issue(lo0 + it + kRing - 1, (it + kRing - 1) % kRing);
+      cp_async_wait<kRing - 1>();
+      const int row = lo0 + it;
+      if (row < hi0) {
+        const int slot = it % kRing;
+#pragma unroll
+        for (int k = 0; k < V; ++k) cur[0][k] = ring[slot][tid * V + k];
+        if (lane == 0) {
+#pragma unroll
+          for (int j = 0; j < R; ++j) edge[par][0][warp + 1][0][j] = cur[0][j];
+        }
+        if (lane == 31) {
+#pragma unroll
+          for (int j = 0; j < R; ++j) edge[par][0][warp + 1][1][j] = cur[0][V - R + j];
+        }
+      }
+    }
+    __syncthreads();
+  };
+
+  int it = 0;
+  for (;;) {
+    bool done = false;
+    // unrolled by E so the accumulator rotation is static
+    [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
+      ((done = done || (it >= n_iter),
+        done ? void() : (body(std::integral_constant<int, Ps>{}, it), ++it, void())),
+       ...);
+    }(std::make_integer_sequence<int, E>{});
+    if (done || it >= n_iter) break;
+  }
+  cp_async_wait<0>();
+}
+
+}  // namespace so2dr_dev

@@ -1,0 +1,100 @@
+// k_misc.cu -- K1 dispatch and the small device kernels:
+//   K6 synthetic init (splitmix64, bit-identical to proj/src/stencil.cpp:91-118).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "k1_launch.h"
+
+namespace so2dr_dev {
+
+int device_sm_count() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cached = n;
+  }
+  return cached;
+}
+
+int k1_max_steps(int dim, int dtype, int kind, int radius) {
+  if (dim == 2) {
+    if (kind == KGRAD) return radius == 1 ? 8 : 0;
+    if (radius < 1 || radius > 4) return 0;
+    if (dtype == 0) return radius == 1 ? 8 : radius == 2 ? 6 : 4;
+    return radius == 1 ? 8 : radius == 2 ? 6 : 2;
+  }
+  if (dim == 3) {
+    if (kind == KGRAD) return 0;
+    if (radius < 1 || radius > 2) return 0;
+    if (dtype == 0) return radius == 1 ? 8 : 4;
+    return radius == 1 ? 4 : 2;
+  }
+  return 0;
+}
+
+cudaError_t k1_launch(const K1Launch& L, cudaStream_t stream) {
+  if (L.dim == 2) return L.dtype == 0 ? launch_k1_2d_f32(L, stream) : launch_k1_2d_f64(L, stream);
+  if (L.dim == 3) return L.dtype == 0 ? launch_k1_3d_f32(L, stream) : launch_k1_3d_f64(L, stream);
+  return cudaErrorInvalidValue;
+}
+
+uint64_t k1_alg_bytes(const K1Launch& L) {
+  const int top_in = std::min(L.base + L.rows, L.y1 + L.radius * L.steps);
+  const int bot_in = std::max(L.base, L.y0 - L.radius * L.steps);
+  const uint64_t unit = static_cast<uint64_t>(L.dim == 3 ? (int64_t)L.plane_rows * L.cols : L.cols) *
+                        (L.dtype == 1 ? 8 : 4);
+  return static_cast<uint64_t>((top_in - bot_in) + (L.y1 - L.y0)) * unit;
+}
+
+// ---- K6: synthetic init ----------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+template <typename T>
+__global__ void init_kernel(T* out, int64_t pitch, int p, int dim, int64_t lo, int64_t n_units,
+                            uint64_t seed) {
+  // one thread per cell of units [lo, lo + n_units); unit = row (2D) / plane (3D)
+  const int64_t rows_per_unit = dim == 3 ? p : 1;
+  const int64_t total_rows = n_units * rows_per_unit;
+  for (int64_t row = blockIdx.y; row < total_rows; row += gridDim.y) {
+    const int64_t unit = lo + row / rows_per_unit;
+    const int y = dim == 3 ? static_cast<int>(row % rows_per_unit) : static_cast<int>(unit);
+    const uint64_t s = dim == 3 ? seed ^ (static_cast<uint64_t>(static_cast<uint32_t>(unit)) *
+                                          0x9E3779B97F4A7C15ULL)
+                                : seed;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < p; x += gridDim.x * blockDim.x) {
+      const uint64_t key = (static_cast<uint64_t>(static_cast<uint32_t>(y)) << 32) |
+                           static_cast<uint32_t>(x);
+      const float v = static_cast<float>(mix64(s ^ mix64(key)) >> 40) * 0x1p-24f;
+      out[row * pitch + x] = static_cast<T>(v);
+    }
+  }
+}
+
+cudaError_t launch_init(int dtype, void* out, int64_t pitch, int p, int dim, int64_t lo,
+                        int64_t n_units, uint64_t seed, cudaStream_t stream) {
+  const int64_t rows = n_units * (dim == 3 ? p : 1);
+  dim3 block(256);
+  dim3 grid(static_cast<unsigned>(std::min<int64_t>((p + 255) / 256, 64)),
+            static_cast<unsigned>(std::min<int64_t>(rows, 65535)));
+  if (rows <= 0) return cudaSuccess;
+  if (dtype == 0)
+    init_kernel<float><<<grid, block, 0, stream>>>(static_cast<float*>(out), pitch, p, dim, lo,
+                                                   n_units, seed);
+  else
+    init_kernel<double><<<grid, block, 0, stream>>>(static_cast<double*>(out), pitch, p, dim, lo,
+                                                    n_units, seed);
+  return cudaGetLastError();
+}
+
+}  // namespace so2dr_dev

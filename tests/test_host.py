@@ -1,0 +1,236 @@
+"""CPU-only tests: the oracle pinned against the reference's golden vectors,
+the host-side model (geometry, closed-form ledgers, modeled arena, kernel
+accounting) against the reference's own outputs, and the C ABI surface.
+No device calls here."""
+import base64
+import json
+import os
+import re
+import zlib
+
+import numpy as np
+import pytest
+
+import paper_2309_08864_b200 as so2dr
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+STENCILS = {"box2d1r": (0, 1), "box2d2r": (0, 2), "box2d3r": (0, 3), "box2d4r": (0, 4),
+            "gradient2d": (1, 1), "star2d1r": (0, 1)}
+
+
+def _weights(o, name):
+    kind, r = STENCILS[name]
+    if name.startswith("star"):
+        return kind, r, o.star_weights(r)
+    return kind, r, o.box_weights(r)
+
+
+def _unpack(s, shape):
+    return np.frombuffer(zlib.decompress(base64.b64decode(s)), dtype=np.float32).reshape(shape)
+
+
+# ----------------------------------------------------------------- oracle --
+
+def test_oracle_cell_values(oracle):
+    for seed, y, x, want in GOLD["cell_value"]:
+        assert float.hex(float(oracle.lib().orc_cell_value(seed, y, x))) == want
+    # SURVEY 8(c) KATs
+    assert float.hex(float(oracle.lib().orc_cell_value(42, 0, 0))) == "0x1.366cfc0000000p-2"
+
+
+@pytest.mark.parametrize("case", GOLD["small_grids"], ids=lambda c: f"{c['stencil']}-{c['sz']}")
+def test_oracle_small_grids_bit_exact(oracle, case):
+    kind, r, w = _weights(oracle, case["stencil"])
+    g = oracle.init_grid(case["sz"], r, case["seed"])
+    assert oracle.fnv1a(g) == case["in_fnv"]
+    out = oracle.run(g, kind, r, w, case["n"])
+    want = _unpack(case["out"], g.shape)
+    assert (out.view(np.uint32) == want.view(np.uint32)).all()
+    assert oracle.fnv1a(out) == case["out_fnv"]
+
+
+@pytest.mark.parametrize("case", [c for c in GOLD["checksums"] if c["sz"] <= 512],
+                         ids=lambda c: f"{c['stencil']}-{c['sz']}")
+def test_oracle_desk_checksums(oracle, case):
+    kind, r, w = _weights(oracle, case["stencil"])
+    g = oracle.init_grid(case["sz"], r, case["seed"])
+    assert oracle.fnv1a(g) == case["in_fnv"]
+    assert oracle.fnv1a(oracle.run(g, kind, r, w, case["n"])) == case["out_fnv"]
+
+
+def test_oracle_config1_checksum(oracle):
+    case = next(c for c in GOLD["checksums"] if c["stencil"] == "star2d1r" and c["sz"] == 4096)
+    assert case["out_fnv"] == 0x2792BA9BAAEE3B83
+    kind, r, w = _weights(oracle, "star2d1r")
+    g = oracle.init_grid(4096, 1, 42)
+    out = oracle.run(g, oracle.STAR, 1, w, 8)  # the star kernel's on-axis chain == box with zero corners
+    assert oracle.fnv1a(out) == case["out_fnv"]
+    assert float.hex(float(out[1, 1])) == case["cell_1_1"]
+
+
+def test_oracle_known_answers(oracle):
+    # proj/tests/test_stencil.cpp:56-145 (also for fp64 and the 3D restatement)
+    ones = np.ones(9)
+    for dt in (np.float32, np.float64):
+        g = np.ones((8, 8), dt)
+        out = oracle.run(g, oracle.BOX, 1, ones, 1)
+        assert (out[1:-1, 1:-1] == 9.0).all()
+        imp = np.zeros((13, 13), dt)
+        imp[6, 6] = 1
+        two = oracle.run(imp, oracle.BOX, 1, ones, 2)
+        prof = np.array([1, 2, 3, 2, 1], dt)
+        assert (two[4:9, 4:9] == np.outer(prof, prof)).all()
+        ident = np.zeros(9)
+        ident[4] = 1
+        g = oracle.init_grid(10, 1, 3, 2, dt)
+        assert (oracle.run(g, oracle.BOX, 1, ident, 3) == g).all()
+    g3 = np.ones((7, 7, 7), np.float32)
+    assert (oracle.run(g3, oracle.BOX, 1, np.ones(27), 1)[1:-1, 1:-1, 1:-1] == 27.0).all()
+
+
+def test_oracle_3d_degenerate_equals_2d_planes(oracle):
+    """3D restatement pinned to 2D: with every dz != 0 weight zero, each z-plane
+    evolves exactly as the 2D reference on that plane."""
+    r, sz, n = 1, 20, 4
+    w2 = oracle.box_weights(1)
+    w3 = np.zeros(27)
+    w3[9:18] = w2
+    g3 = oracle.init_grid(sz, r, 5, 3)
+    out3 = oracle.run(g3, oracle.BOX, r, w3, n)
+    for z in range(r, r + sz):
+        plane = oracle.run(g3[z].copy(), oracle.BOX, r, w2, n)
+        assert (out3[z].view(np.uint32) == plane.view(np.uint32)).all()
+    assert (oracle.init_grid(sz, r, 5, 3)[0] == oracle.init_grid(sz, r, 5, 2)).all()
+
+
+def test_oracle_matches_compiled_reference(oracle):
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built on this machine")
+    import ctypes
+
+    R = oracle.ref()
+    for kind, r in [(0, 1), (0, 2), (0, 3), (0, 4), (1, 1)]:
+        g = oracle.init_grid(37, r, 99)
+        ref = np.empty_like(g)
+        err = ctypes.create_string_buffer(128)
+        assert R.ref_run_reference(kind, r, None, 37, r, g.ctypes.data, 6, ref.ctypes.data, err, 128) == 0
+        mine = oracle.run(g, kind, r, oracle.box_weights(r), 6)
+        assert (mine.view(np.uint32) == ref.view(np.uint32)).all()
+
+
+# ------------------------------------------------------------- host model --
+
+def test_abi_exports_every_header_symbol():
+    L = so2dr.lib()
+    hdr = open(os.path.join(ROOT, "include", "so2dr_cuda.h")).read()
+    names = set(re.findall(r"\b(so2dr_[a-z0-9_]+)\s*\(", hdr))
+    assert len(names) >= 25
+    for n in sorted(names):
+        assert hasattr(L, n), n
+    assert set(so2dr.EXPORTS) <= names
+    assert L.so2dr_abi_version() == 1
+
+
+def test_no_device_here_fails_loudly():
+    if so2dr.device_count() > 0:
+        pytest.skip("a device is present")
+    with pytest.raises(so2dr.DeviceError):
+        so2dr.Engine(0)
+
+
+def test_plan_chunks_worked_example():
+    # proj/tests/test_layout.cpp:17-39
+    fence, ch = so2dr.plan_chunks(so2dr.RunConfig(sz=16, r=1, d=4, s_tb=2, k_on=1, n=2))
+    assert fence == [1, 5, 9, 13, 17]
+    assert [c["transfer"][1] - c["transfer"][0] for c in ch] == [7, 4, 4, 3]
+    assert ch[0]["transfer"] == (0, 7) and ch[3]["transfer"] == (15, 18)
+    assert ch[1]["shared_in"] == (3, 7)
+    assert ch[1]["working"] == (3, 11) and ch[3]["working"] == (11, 18)
+    with pytest.raises(so2dr.InfeasibleError) as e:
+        so2dr.plan_chunks(so2dr.RunConfig(sz=16, r=1, d=4, s_tb=3, k_on=1, n=3))
+    assert e.value.constraint == "W_halo*S_TB <= D_chk"
+    with pytest.raises(so2dr.InvalidSpecError):
+        so2dr.plan_chunks(so2dr.RunConfig(sz=15, r=1, d=4, s_tb=1, k_on=1, n=1))
+
+
+def test_transfer_rows_tile_the_grid():
+    # proj/tests/test_layout.cpp:57-86
+    for sz in range(8, 65, 8):
+        for d in (2, 4, 8):
+            for r in range(1, 5):
+                s = 1
+                while 2 * r * s <= sz // d:
+                    _, ch = so2dr.plan_chunks(so2dr.RunConfig(sz=sz, r=r, d=d, s_tb=s, k_on=1, n=s))
+                    cur = 0
+                    for c in ch:
+                        assert c["transfer"][0] == cur
+                        cur = c["transfer"][1]
+                    assert cur == sz + 2 * r
+                    s += 1
+
+
+@pytest.mark.parametrize("case", GOLD["expected_ledger"], ids=lambda c: f"{c['mode']}-{c['cfg'][0]}-{c['cfg'][1]}")
+def test_expected_ledger_matches_reference(case):
+    cfg = so2dr.RunConfig(*case["cfg"])
+    kp = so2dr.KernelPlan(*case["kp"])
+    got = so2dr.expected_ledger(case["mode"], cfg, kp)
+    keys = ("htod", "dtoh", "ondevice", "kernel_invocations", "rounds", "redundant_updates")
+    assert [got[k] for k in keys] == case["expected"]
+    assert got["redundancy_exact"] == case["exact"]
+    if "arena_bytes" in case:
+        assert so2dr.arena_bytes(cfg, kp) == case["arena_bytes"]
+
+
+@pytest.mark.parametrize("case", GOLD["fused_stats"], ids=lambda c: f"{c['region']}-{c['steps']}-{c['tile']}")
+def test_kernel_stats_match_reference(case):
+    st = so2dr.kernel_stats(case["r"], case["steps"], case["tile"], case["region"], case["interior"],
+                            case["region"], case["rows"][0], case["rows"][1], case["cols"])
+    assert [st["scratch_load"], st["scratch_store"], st["updates"], st["redundant"]] == case["stats"]
+
+
+def test_kernel_stats_reference_unit_cases():
+    # proj/tests/test_engine.cpp:34-65
+    st = so2dr.kernel_stats(1, 2, 8, (20, 36, 20, 36), (1, 63, 1, 63), (20, 36, 20, 36), 0, 64, 64)
+    assert st["scratch_load"] == 4 * 144 * 4 and st["scratch_store"] == 4 * 64 * 4
+    assert st["updates"] == 4 * 100 + 4 * 64 and st["redundant"] == st["updates"] - 2 * 256
+    st = so2dr.kernel_stats(1, 1, 64, (10, 26, 8, 40), (1, 63, 1, 63), (10, 26, 8, 40), 0, 64, 64)
+    assert st == {"scratch_load": 18 * 34 * 4, "scratch_store": 16 * 32 * 4, "updates": 16 * 32, "redundant": 0}
+
+
+def test_kernel_stats_closed_form_equals_tile_loop():
+    """The large-width closed form (used for 92k-column chunks) equals the literal tile loop."""
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        cols = int(rng.integers(100, 3000))
+        r = int(rng.integers(1, 5))
+        s = int(rng.integers(1, 9))
+        tile = int(rng.integers(1, 40))
+        x0 = int(rng.integers(0, cols - 1))
+        x1 = int(rng.integers(x0 + 1, cols + 1))
+        y0, y1 = 10, 20
+        region = (y0, y1, x0, x1)
+        st = so2dr.kernel_stats(r, s, tile, region, (r, 1000, r, cols - r), region, 0, 1000, cols)
+        # literal loop (proj/src/kernels.cpp:62-109)
+        e0 = r * s
+        lx = sum(min(min(a + tile, x1) + e0, cols) - max(a - e0, 0) for a in range(x0, x1, tile))
+        ly = sum(min(min(a + tile, y1) + e0, 1000) - max(a - e0, 0) for a in range(y0, y1, tile))
+        assert st["scratch_load"] == lx * ly * 4
+
+
+def test_engine_ledger_goldens_are_consistent():
+    """Every reference engine ledger in the fixtures satisfies the closed forms
+    (the GPU tests then require equality with these ledgers)."""
+    for e in GOLD["engine"]:
+        cfg = so2dr.RunConfig(*e["cfg"])
+        exp = so2dr.expected_ledger(e["mode"], cfg, so2dr.KernelPlan(*e["kp"]))
+        led = dict(zip(so2dr.LEDGER_FIELDS, e["ledger"]))
+        for k in ("htod", "dtoh", "ondevice", "kernel_invocations", "rounds"):
+            assert led[k] == exp[k], (e["mode"], e["cfg"], k)
+
+
+def test_checksum_helper():
+    a = np.arange(10, dtype=np.float32)
+    import pyoracle
+
+    assert so2dr.grid_checksum(a) == pyoracle.fnv1a(a)
