@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""SO2DR B200 benchmark -- BASELINE.json metric:
+"GCell-updates/s end-to-end (incl. H2D/D2H) at 1/2/4/8 B200; % of roofline".
+
+Workload (BASELINE configs[1]): box2d1r fp32 out-of-core, grid ~2x the device
+budget on one B200, 64 timesteps: sz=92160 (92162^2 fp32 = 33.98 GB host grid),
+16 GiB real HBM budget, d=16 chunks, S_TB=64 (one round), k_on=8, N_strm=3.
+A "step" is one full so2dr run (64 timesteps over the whole grid).
+
+  value : same run with the grid already resident in HBM (copies become D2D)
+  e2e   : the headline -- C-ABI so2dr_run on the pinned HOST grid, all PCIe
+          traffic inside the timed region (CUDA events, first H2D -> last D2H)
+
+Multi-GPU (torchrun): the d chunks are slab-partitioned over ranks (weak scaling:
+each rank streams a ~34 GB slab of a sz~92160*sqrt(N) grid); inter-slab halos
+move GPU-to-GPU over CUDA IPC peer memory. --impl reference times the
+reference CPU solver (oracle/_ref, built from /root/reference) on a bounded
+sample of the same workload.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+os.environ.setdefault("OMP_PROC_BIND", "spread")
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import numpy as np  # noqa: E402
+
+METRIC = "GCell-updates/s end-to-end (incl. H2D/D2H) at 1/2/4/8 B200; % of roofline"
+UNIT = "GCell/s"
+SZ1, D_PER_RANK, S_TB, K_ON, NSTEPS, NSTRM, R = 92160, 16, 64, 8, 64, 3, 1
+BUDGET = 16 << 30
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def geometry(world: int):
+    d = D_PER_RANK * world
+    sz = SZ1 if world == 1 else int(round(SZ1 * math.sqrt(world) / d)) * d
+    return sz, d
+
+
+def workload_desc(world, sz, d):
+    gb = (sz + 2 * R) ** 2 * 4 / 1e9
+    return (f"box2d1r fp32 out-of-core, sz={sz} ({gb:.2f} GB grid, {gb / world / (BUDGET / 1e9):.2f}x the "
+            f"{BUDGET >> 30} GiB per-GPU HBM budget), n={NSTEPS} timesteps, d={d}, S_TB={S_TB}, k_on={K_ON}, "
+            f"N_strm={NSTRM}, slab-partitioned over {world} GPU(s)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def pcie_probe(torch, dev):
+    """Pinned H2D / D2H GB/s, each alone and both at once (per direction)."""
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(n, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    out = {}
+    for name in ("h2d", "d2h", "duplex"):
+        best = 0.0
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            if name in ("h2d", "duplex"):
+                with torch.cuda.stream(s1):
+                    d.copy_(h, non_blocking=True)
+            if name in ("d2h", "duplex"):
+                with torch.cuda.stream(s2):
+                    h2.copy_(d2, non_blocking=True)
+            torch.cuda.synchronize(dev)
+            best = max(best, n / (time.perf_counter() - t0) / 1e9)
+        out[name + "_GBps_per_dir"] = best
+    del h, h2, d, d2
+    return out
+
+
+def cpu_baseline_sample():
+    """The reference's own CPU solver (oracle/_ref = /root/reference sources, -O3
+    -ffp-contract=off -fopenmp) on a bounded sample of the workload: same stencil,
+    d, S_TB, k_on, n; sz reduced 8x (1/64 of the cells)."""
+    import ctypes
+
+    import pyoracle as o
+
+    sz, d = SZ1 // 8, D_PER_RANK
+    cells = (sz + 2 * R) ** 2
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    if o.have_ref():
+        R_ = o.ref()
+        g = np.empty((sz + 2 * R, sz + 2 * R), np.float32)
+        R_.ref_init_grid(sz, R, 42, g.ctypes.data)
+        out = np.empty_like(g)
+        led = (ctypes.c_uint64 * 9)()
+        peak, wall = ctypes.c_uint64(), ctypes.c_double()
+        err = ctypes.create_string_buffer(256)
+        t0 = time.perf_counter()
+        rc = R_.ref_run_engine(0, 0, R, None, (ctypes.c_int * 8)(sz, R, d, S_TB, K_ON, NSTRM, NSTEPS, 2),
+                               (ctypes.c_int * 2)(K_ON, 32), 64 << 20, 1 << 40, 760e9, 15.75e9, 0, 0,
+                               g.ctypes.data, out.ctypes.data, led, ctypes.byref(peak), ctypes.byref(wall), err, 256)
+        t = time.perf_counter() - t0
+        if rc != 0:
+            raise RuntimeError(err.value.decode())
+        sec = wall.value if wall.value > 0 else t
+        return {"value": sz * sz * NSTEPS / sec / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"reference run_engine(so2dr) box2d1r sz={sz} d={d} S_TB={S_TB} k_on={K_ON} n={NSTEPS} "
+                          f"({cells * 4 / 1e9:.2f} GB grid, {sz * sz * NSTEPS / 1e9:.1f} G updates) in {sec:.2f} s; "
+                          f"RunReport.wall_seconds, OMP_NUM_THREADS={cores}, 3 std::thread workers",
+                "seconds": sec}
+    # fallback: the C restatement (serial)
+    g = o.init_grid(sz // 4, R, 42)
+    t0 = time.perf_counter()
+    o.run(g, o.BOX, R, o.box_weights(R), 4)
+    sec = time.perf_counter() - t0
+    s4 = sz // 4
+    return {"value": s4 * s4 * 4 / sec / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle port (serial C) box2d1r sz={s4} n=4 in {sec:.2f} s", "seconds": sec}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    samples = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline_sample()
+        if i >= args.warmup:
+            samples.append(cb)
+    v = statistics.median([s["value"] for s in samples])
+    cb = dict(samples[-1])
+    cb["value"] = v
+    cb.pop("seconds", None)
+    sz, d = geometry(1)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(s["seconds"] for s in samples),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (splitmix64 init_grid, seed 42)",
+            "config": {"workload": workload_desc(1, sz, d) + "; reference CPU solver timed on a bounded sample "
+                       "(sz/8, same d/S_TB/k_on/n)"},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--k-on", type=int, default=K_ON)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-value-leg", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2309_08864_b200 as so2dr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl" if os.environ.get("SO2DR_SHARE_DEVICE") != "1" else "gloo")
+    ndev = torch.cuda.device_count()
+    dev_index = 0 if os.environ.get("SO2DR_SHARE_DEVICE") == "1" else local % max(ndev, 1)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+
+    k_on = args.k_on
+    sz, d = geometry(world)
+    cfg = so2dr.RunConfig(sz=sz, r=R, d=d, s_tb=S_TB, k_on=k_on, n_strm=NSTRM, n=NSTEPS)
+    spec = so2dr.StencilSpec.box(R)
+    kp = so2dr.KernelPlan(k_on, 32, 64 << 20)
+    eng = so2dr.Engine(dev_index, BUDGET)
+    lo, hi = so2dr.slab_rows(cfg, rank, world)
+    p = sz + 2 * R
+    shape = (hi - lo, p)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def connect():
+        if world == 1:
+            return
+        blob = eng.slab_prepare(spec, cfg, np.float32, rank, world)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, blob)
+        eng.slab_connect(blobs[rank - 1] if rank > 0 else None, blobs[rank + 1] if rank < world - 1 else None)
+
+    def run_once(grid):
+        if world == 1:
+            rep = eng.run("so2dr", grid, spec, cfg, kp, diag=False)
+            return rep.timing, rep.ledger
+        led, tim = eng.slab_run(spec, cfg, grid, kp)
+        return tim, led
+
+    def leg(grid, steps, warmup):
+        for _ in range(warmup):
+            run_once(grid)
+        barrier()
+        times, kms, kmax, launches, algb, h2d, d2h = [], 0.0, 0.0, 0, 0, 0, 0
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            tim, led = run_once(grid)
+            times.append(tim["device_ms"])
+            kms += tim["kernel_ms"]
+            kmax = max(kmax, tim["kernel_max_ms"])
+            launches += tim["kernel_launches"]
+            algb += tim["kernel_alg_bytes"]
+            h2d += tim["h2d_bytes"]
+            d2h += tim["d2h_bytes"]
+        barrier()
+        wall = time.perf_counter() - t0
+        dev_ms = allmax(sum(times))
+        return {"device_ms_total": dev_ms, "wall_s": allmax(wall), "kernel_ms": kms, "kernel_max_ms": kmax,
+                "launches": launches, "alg_bytes": algb, "h2d": h2d, "d2h": d2h, "per_step_ms": times}
+
+    total_updates = sz * sz * NSTEPS  # per step, whole job
+
+    # ---- value leg: grid resident in HBM ---------------------------------
+    value_res = None
+    if not args.no_value_leg:
+        gdev = torch.empty(shape, dtype=torch.float32, device=dev)
+        eng.init_rows(sz, R, 42, lo, hi, gdev)
+        connect()
+        value_res = leg(gdev, args.steps, args.warmup)
+        del gdev
+        torch.cuda.empty_cache()
+
+    # ---- e2e leg: pinned host grid through the C ABI ------------------------
+    host = np.empty(shape, dtype=np.float32)
+    t0 = time.perf_counter()
+    eng.host_register(host)
+    t_reg = time.perf_counter() - t0
+    eng.init_rows(sz, R, 42, lo, hi, host)
+    connect()
+    pc = pcie_probe(torch, dev) if rank == 0 else {}
+    with ClockSampler(dev_index) as clk:
+        e2e_res = leg(host, args.steps, args.warmup)
+    clocks = clk.summary()
+
+    if rank != 0:
+        eng.host_unregister(host)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    e2e_v = total_updates * args.steps / (e2e_res["device_ms_total"] / 1e3) / 1e9
+    val_v = (total_updates * args.steps / (value_res["device_ms_total"] / 1e3) / 1e9) if value_res else None
+    # K1 roofline: algorithmic bytes (input rows read once + output rows written once per launch)
+    kr = e2e_res
+    k_gbs = kr["alg_bytes"] / (kr["kernel_ms"] / 1e3) / 1e9 if kr["kernel_ms"] > 0 else 0.0
+    per_launch = kr["alg_bytes"] / max(kr["launches"], 1)
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))
+        if prof.get("k_on") == k_on:
+            traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    bw_dir = pc.get("duplex_GBps_per_dir", 50.0)
+    r_pcie = world * bw_dir * 1e9 * S_TB / 4 / 1e9
+    r_hbm = world * hbm * 1e9 / (2 * 4 / k_on + 2 * 4 / S_TB) / 1e9
+    r_bind = min(r_pcie, r_hbm)
+    cb = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline_sample()
+            cb.pop("seconds", None)
+        except Exception as e:  # never fail the GPU line on the baseline
+            cb = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference", "sample": f"failed: {e}"}
+    line = {
+        "metric": METRIC, "value": val_v if val_v is not None else e2e_v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": e2e_res["device_ms_total"] / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (splitmix64 init_grid, seed 42; grid generated on device)",
+        "config": {"workload": workload_desc(world, sz, d), "sz": sz, "d": d, "s_tb": S_TB, "k_on": k_on,
+                   "n": NSTEPS, "n_strm": NSTRM, "budget_bytes_per_gpu": BUDGET,
+                   "grid_bytes": (sz + 2 * R) ** 2 * 4,
+                   "l2": "no flush needed: every step streams the whole grid (>= 34 GB >> 126 MB L2)",
+                   "value_leg": "same so2dr run with the grid resident in HBM (transfers become D2D)",
+                   "timing": "CUDA events on the engine streams, first H2D enqueue -> last D2H completion, "
+                             "summed over steps, max over ranks"},
+        "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": e2e_res["h2d"] // args.steps,
+                "d2h_bytes_per_step": e2e_res["d2h"] // args.steps,
+                "wall_s_per_step": e2e_res["wall_s"] / args.steps},
+        "roofline": {"bound": "hbm", "kernel": "K1 k1_stencil2d<float,1,%d,box>" % k_on, "achieved": k_gbs,
+                     "peak": hbm, "unit": "GB/s", "frac": k_gbs / hbm, "traffic": traffic,
+                     "alg_bytes_per_launch": per_launch,
+                     "avg_launch_ms": kr["kernel_ms"] / max(kr["launches"], 1),
+                     "kernel_share_of_step": kr["kernel_ms"] / max(e2e_res["device_ms_total"], 1e-9),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+        "binding_roofline": {"R_pcie": r_pcie, "R_hbm": r_hbm, "R_bind": r_bind, "unit": UNIT,
+                             "frac_e2e": e2e_v / r_bind, "frac_value_vs_R_hbm": (val_v / r_hbm) if val_v else None,
+                             "pcie_measured": pc,
+                             "formula": "R_pcie = G*BW_pcie_dir(duplex)*S_TB/b ; R_hbm = G*BW_hbm/(2b/k_on + 2b/S_TB)"},
+        "cpu_baseline": cb,
+        "clocks": clocks,
+        "gpu_launches": e2e_res["launches"],
+        "host_register_s": t_reg,
+    }
+    print(json.dumps(line), flush=True)
+    eng.host_unregister(host)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

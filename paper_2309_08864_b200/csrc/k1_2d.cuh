@@ -85,27 +85,26 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <typename T, int V>
-struct VecIO;
-template <>
-struct VecIO<float, 4> {
-  static __device__ __forceinline__ void store(float* p, const float (&v)[4]) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  }
-};
-template <>
-struct VecIO<double, 2> {
-  static __device__ __forceinline__ void store(double* p, const double (&v)[2]) {
-    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
-  }
-};
-template <>
-struct VecIO<double, 4> {
-  static __device__ __forceinline__ void store(double* p, const double (&v)[4]) {
-    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
-    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
-  }
-};
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES)
+                 : "memory");
+}
+
+// BYTES-wide vector store of consecutive elements
+template <int BYTES>
+__device__ __forceinline__ void store_vec(void* dst, const void* src) {
+  if constexpr (BYTES == 16)
+    *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
+  else if constexpr (BYTES == 8)
+    *reinterpret_cast<float2*>(dst) = *reinterpret_cast<const float2*>(src);
+  else
+    *reinterpret_cast<float*>(dst) = *reinterpret_cast<const float*>(src);
+}
 
 // Pipeline depth of the cp.async input ring.
 constexpr int kRing = 4;
@@ -115,17 +114,18 @@ struct K1Plan2D {
   static constexpr int E = 2 * R + 1;
   static constexpr int H = R * S;
   static constexpr int NW = NT / 32;
-  static constexpr int VEC = 16 / (int)sizeof(T);
-  static_assert(V % VEC == 0, "V must be a whole number of 16-byte vectors");
+  static constexpr int CPB = (V * (int)sizeof(T)) >= 16 ? 16 : V * (int)sizeof(T);  // copy bytes
+  static constexpr int VEC = CPB / (int)sizeof(T);  // elements per copy / alignment unit
+  static_assert(V % VEC == 0, "V must be a whole number of copy vectors");
   static_assert(R <= V, "warp-shuffle halo needs R <= V");
   static constexpr int NACC = (KIND == KGRAD) ? 0 : S;
   static constexpr int NGR = (KIND == KGRAD) ? S : 0;
 };
 
-template <typename T, int R, int S, int KIND, int V, int NT>
-__global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
+template <typename T, int R, int S, int KIND, int V, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
   using P = K1Plan2D<T, R, S, KIND, V, NT>;
-  constexpr int E = P::E, H = P::H, NW = P::NW, VEC = P::VEC;
+  constexpr int E = P::E, H = P::H, NW = P::NW, VEC = P::VEC, CPB = P::CPB;
 
   __shared__ __align__(16) T ring[kRing][NT * V];
   // warp-edge halo values: [parity][producer stage][warp + 1][side][R]
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
     const int x = xt + k;
     if (x < a.ix0 || x >= a.ix1) ringmask |= 1u << k;
   }
-  // whole 16-byte vectors inside [0, pitch) are loaded (a thread may straddle
+  // whole copy vectors inside [0, pitch) are loaded (a thread may straddle
   // column 0 when V > VEC, e.g. fp64 with V=4)
   const bool load_ok = xt + V > 0 && xt < a.pitch;
   bool store_full = true, store_any = false;
@@ -170,18 +170,16 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
     store_full = store_full && ok;
     store_any = store_any || ok;
   }
+  // CTA-uniform: does any thread own a pass-through column?
+  const bool cta_ring = tc0 < a.ix0 || tc0 + NT * V > a.ix1;
 
   // zero the edge buffers so out-of-strip halo reads are finite garbage
   for (int i = tid; i < 2 * S * (NW + 2) * 2 * R; i += NT) (&edge[0][0][0][0][0])[i] = T(0);
 
-  T wt[E * E];
-#pragma unroll
-  for (int i = 0; i < E * E; ++i) wt[i] = a.w[i];
-
   // carried state
-  T cur[S][V];                                   // stage 0..S-1 emitted row (own cells)
-  T acc[P::NACC > 0 ? P::NACC : 1][E][V];        // box/star partial accumulators
-  T grow[P::NGR > 0 ? P::NGR : 1][3][V + 2];     // gradient row window (with x halo)
+  T cur[S][V];                                // stage 0..S-1 emitted row (own cells)
+  T acc[P::NACC > 0 ? P::NACC : 1][E][V];     // box/star partial accumulators
+  T grow[P::NGR > 0 ? P::NGR : 1][3][V + 2];  // gradient row window (with x halo)
 #pragma unroll
   for (int u = 0; u < S; ++u)
 #pragma unroll
@@ -193,7 +191,7 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
       const T* src = a.in + (int64_t)(row - sy0) * a.pitch + xt;
 #pragma unroll
       for (int v = 0; v < V; v += VEC)
-        if (xt + v >= 0) cp_async16(&ring[slot][tid * V + v], src + v);
+        if (xt + v >= 0) cp_async<CPB>(&ring[slot][tid * V + v], src + v);
     }
     cp_async_commit();
   };
@@ -211,9 +209,12 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
     return __ldg(gin + (int64_t)(row - sy0) * a.pitch + x);
   };
 
-  // One pipeline iteration at compile-time phase PH = it mod E.
-  auto body = [&](auto phase_tag, int it) {
+  // One pipeline iteration at compile-time phase PH = it mod E. FAST = steady
+  // state: every stage consumes and emits an interior row and the CTA owns no
+  // pass-through column, so all range checks compile away.
+  auto body = [&](auto phase_tag, auto fast_tag, int it) {
     constexpr int PH = decltype(phase_tag)::value;
+    constexpr bool FAST = decltype(fast_tag)::value;
     const int par = it & 1, ppar = par ^ 1;
 
     // stages in descending order: stage u consumes cur[u-1] (emitted by stage
@@ -222,8 +223,8 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
     for (int u = S; u >= 1; --u) {
       const int A = it + lo0 - u - (u - 1) * R;  // row consumed by stage u
       const int Erow = A - R;                    // row emitted by stage u
-      const bool consume = A >= lo[u - 1] && A < hi[u - 1];
-      const bool emit = Erow >= lo[u] && Erow < hi[u];
+      const bool consume = FAST || (A >= lo[u - 1] && A < hi[u - 1]);
+      const bool emit = FAST || (Erow >= lo[u] && Erow < hi[u]);
       if (!consume && !emit) continue;
 
       T seg[V + 2 * R];
@@ -265,22 +266,22 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
         if (consume) {
 #pragma unroll
           for (int m = 0; m < E; ++m) {
-            const int dy = m - R;                    // A contributes at dy to row A-dy
-            const int sl = (PH - m + 2 * E) % E;     // slot of output row A+R-m
+            const int dy = m - R;                 // A contributes at dy to row A-dy
+            const int sl = (PH - m + 2 * E) % E;  // slot of output row A+R-m
 #pragma unroll
             for (int k = 0; k < V; ++k) {
               T x = (m == 0) ? T(0) : acc[u - 1][sl][k];
               if constexpr (KIND == KBOX) {
 #pragma unroll
                 for (int dx = -R; dx <= R; ++dx)
-                  x = fma_rn(wt[(dy + R) * E + dx + R], seg[R + k + dx], x);
+                  x = fma_rn(a.w[(dy + R) * E + dx + R], seg[R + k + dx], x);
               } else {  // star: on-axis taps only
                 if (dy != 0) {
-                  x = fma_rn(wt[(dy + R) * E + R], seg[R + k], x);
+                  x = fma_rn(a.w[(dy + R) * E + R], seg[R + k], x);
                 } else {
 #pragma unroll
                   for (int dx = -R; dx <= R; ++dx)
-                    x = fma_rn(wt[R * E + dx + R], seg[R + k + dx], x);
+                    x = fma_rn(a.w[R * E + dx + R], seg[R + k + dx], x);
                 }
               }
               acc[u - 1][sl][k] = x;
@@ -295,18 +296,21 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
       }
 
       if (emit) {
-        if (Erow < a.iy0 || Erow >= a.iy1) {
+        if constexpr (!FAST) {
+          if (Erow < a.iy0 || Erow >= a.iy1) {
 #pragma unroll
-          for (int k = 0; k < V; ++k) outv[k] = passthru(Erow, k);
-        } else if (ringmask) {
+            for (int k = 0; k < V; ++k) outv[k] = passthru(Erow, k);
+          } else if (ringmask) {
 #pragma unroll
-          for (int k = 0; k < V; ++k)
-            if (ringmask & (1u << k)) outv[k] = passthru(Erow, k);
+            for (int k = 0; k < V; ++k)
+              if (ringmask & (1u << k)) outv[k] = passthru(Erow, k);
+          }
         }
         if (u == S) {
           T* dst = gout + (int64_t)(Erow - sy0) * a.pitch + xt;
           if (store_full) {
-            VecIO<T, V>::store(dst, outv);
+#pragma unroll
+            for (int v = 0; v < V; v += VEC) store_vec<CPB>(dst + v, &outv[v]);
           } else if (store_any) {
 #pragma unroll
             for (int k = 0; k < V; ++k)
@@ -331,8 +335,7 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
     {
       issue(lo0 + it + kRing - 1, (it + kRing - 1) % kRing);
       cp_async_wait<kRing - 1>();
-      const int row = lo0 + it;
-      if (row < hi0) {
+      if (FAST || lo0 + it < hi0) {
         const int slot = it % kRing;
 #pragma unroll
         for (int k = 0; k < V; ++k) cur[0][k] = ring[slot][tid * V + k];
@@ -349,17 +352,39 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil2d(const K1Args2D<T> a) {
     __syncthreads();
   };
 
-  int it = 0;
-  for (;;) {
-    bool done = false;
-    // unrolled by E so the accumulator rotation is static
-    [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
-      ((done = done || (it >= n_iter),
-        done ? void() : (body(std::integral_constant<int, Ps>{}, it), ++it, void())),
-       ...);
-    }(std::make_integer_sequence<int, E>{});
-    if (done || it >= n_iter) break;
+  // ---- steady-state window [f_lo, f_hi): every stage consumes a stored row
+  // and emits an interior row, stage 0 still has rows to load.
+  int f_lo = 0, f_hi = hi0 - lo0;
+#pragma unroll
+  for (int u = 1; u <= S; ++u) {
+    const int c = lo0 - u - (u - 1) * R;  // A_u(it) = it + c
+    f_lo = max(f_lo, lo[u - 1] - c);
+    f_hi = min(f_hi, hi[u - 1] - c);
+    f_lo = max(f_lo, max(lo[u], a.iy0) + R - c);
+    f_hi = min(f_hi, min(hi[u], a.iy1) + R - c);
   }
+  if (cta_ring) f_hi = f_lo;
+
+  int it = 0;
+  auto run_general = [&](int stop) {
+    while (it < stop) {
+      [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
+        ((it < stop ? (body(std::integral_constant<int, Ps>{}, std::false_type{}, it), ++it, void())
+                    : void()),
+         ...);
+      }(std::make_integer_sequence<int, E>{});
+    }
+  };
+  const int fl = (f_lo + E - 1) / E * E;  // phase-aligned start of the fast loop
+  if (f_hi - fl >= E) {
+    run_general(fl);
+    while (it + E <= f_hi) {
+      [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
+        ((body(std::integral_constant<int, Ps>{}, std::true_type{}, it), ++it), ...);
+      }(std::make_integer_sequence<int, E>{});
+    }
+  }
+  run_general(n_iter);
   cp_async_wait<0>();
 }
 

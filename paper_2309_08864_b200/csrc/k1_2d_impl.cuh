@@ -3,6 +3,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 
@@ -13,23 +14,34 @@ namespace so2dr_dev {
 
 constexpr int kThreads2D = 256;
 
+// cells per thread (V) and the launch-bounds occupancy target per shape
 template <typename T>
 constexpr int v2d(int R) {
   return sizeof(T) == 4 ? 4 : (R <= 2 ? 2 : 4);
 }
 template <typename T>
 constexpr int maxs2d(int R) {
-  return sizeof(T) == 4 ? (R == 1 ? 8 : R == 2 ? 6 : 4) : (R == 1 ? 8 : R == 2 ? 6 : 2);
+  return sizeof(T) == 4 ? (R == 1 ? 8 : R == 2 ? 6 : 4) : (R == 1 ? 8 : R == 2 ? 6 : R == 3 ? 2 : 1);
 }
 
 inline int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
-template <typename T, int R, int S, int KIND>
+// Tuning knob for experiments: SO2DR_K1_V=2 selects the 2-cell-per-thread
+// variant of the fp32 radius-1 kernels (default 4).
+inline int k1_v_override() {
+  static int v = [] {
+    const char* s = std::getenv("SO2DR_K1_V");
+    return s ? std::atoi(s) : 0;
+  }();
+  return v;
+}
+
+template <typename T, int R, int S, int KIND, int V, int MINB>
 cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
-  constexpr int V = v2d<T>(R);
   constexpr int NT = kThreads2D;
   constexpr int H = R * S;
-  constexpr int VEC = 16 / (int)sizeof(T);
+  using P = K1Plan2D<T, R, S, KIND, V, NT>;
+  constexpr int VEC = P::VEC;
   K1Args2D<T> a;
   a.in = static_cast<const T*>(L.in);
   a.out = static_cast<T*>(L.out);
@@ -49,17 +61,17 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   const int width = L.x1 - (a.xorg + H);
   const int nx = std::max(1, (width + a.strip - 1) / a.strip);
   const int height = L.y1 - L.y0;
-  // y segments: enough CTAs for ~4 waves at one CTA per SM, but keep each
+  // y segments: enough CTAs for ~4 waves at MINB CTAs per SM, but keep each
   // segment long against its R*S warm-up + S*(R+1) pipeline fill.
   const int sms = device_sm_count();
   const int min_seg = std::max(48, 6 * (H + S * (R + 1)));
   const int max_ny = std::max(1, height / min_seg);
-  int ny = std::max(1, (4 * sms + nx - 1) / nx);
+  int ny = std::max(1, (4 * MINB * sms + nx - 1) / nx);
   ny = std::min(ny, max_ny);
   a.seg = (height + ny - 1) / ny;
   ny = (height + a.seg - 1) / a.seg;
   dim3 grid(nx, ny);
-  k1_stencil2d<T, R, S, KIND, V, NT><<<grid, NT, 0, stream>>>(a);
+  k1_stencil2d<T, R, S, KIND, V, NT, MINB><<<grid, NT, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -68,36 +80,37 @@ cudaError_t launch_2d_s(const K1Launch& L, cudaStream_t stream) {
   if constexpr (S > maxs2d<T>(R)) {
     return cudaErrorInvalidValue;
   } else {
-    if (L.steps == S) return launch_2d_fixed<T, R, S, KIND>(L, stream);
+    if (L.steps == S) {
+      if constexpr (sizeof(T) == 4 && R == 1 && KIND != KGRAD) {
+        if (k1_v_override() == 2) return launch_2d_fixed<T, R, S, KIND, 2, 2>(L, stream);
+      }
+      return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1>(L, stream);
+    }
     return launch_2d_s<T, R, KIND, S + 1>(L, stream);
   }
 }
 
-template <typename T>
-cudaError_t launch_2d(const K1Launch& L, cudaStream_t stream) {
+template <typename T, int R>
+cudaError_t launch_2d_r(const K1Launch& L, cudaStream_t stream) {
   if (L.steps < 1) return cudaErrorInvalidValue;
   switch (L.kind) {
     case KGRAD:
-      if (L.radius != 1) return cudaErrorInvalidValue;
-      return launch_2d_s<T, 1, KGRAD>(L, stream);
-    case KBOX:
-      switch (L.radius) {
-        case 1: return launch_2d_s<T, 1, KBOX>(L, stream);
-        case 2: return launch_2d_s<T, 2, KBOX>(L, stream);
-        case 3: return launch_2d_s<T, 3, KBOX>(L, stream);
-        case 4: return launch_2d_s<T, 4, KBOX>(L, stream);
-      }
-      break;
-    case KSTAR:
-      switch (L.radius) {
-        case 1: return launch_2d_s<T, 1, KSTAR>(L, stream);
-        case 2: return launch_2d_s<T, 2, KSTAR>(L, stream);
-        case 3: return launch_2d_s<T, 3, KSTAR>(L, stream);
-        case 4: return launch_2d_s<T, 4, KSTAR>(L, stream);
-      }
-      break;
+      if constexpr (R == 1) return launch_2d_s<T, 1, KGRAD>(L, stream);
+      return cudaErrorInvalidValue;
+    case KBOX: return launch_2d_s<T, R, KBOX>(L, stream);
+    case KSTAR: return launch_2d_s<T, R, KSTAR>(L, stream);
   }
   return cudaErrorInvalidValue;
 }
+
+// per-(type, radius) entry points, each compiled in its own translation unit
+cudaError_t launch_k1_2d_f32_r1(const K1Launch& L, cudaStream_t s);
+cudaError_t launch_k1_2d_f32_r2(const K1Launch& L, cudaStream_t s);
+cudaError_t launch_k1_2d_f32_r3(const K1Launch& L, cudaStream_t s);
+cudaError_t launch_k1_2d_f32_r4(const K1Launch& L, cudaStream_t s);
+cudaError_t launch_k1_2d_f64_r1(const K1Launch& L, cudaStream_t s);
+cudaError_t launch_k1_2d_f64_r2(const K1Launch& L, cudaStream_t s);
+cudaError_t launch_k1_2d_f64_r3(const K1Launch& L, cudaStream_t s);
+cudaError_t launch_k1_2d_f64_r4(const K1Launch& L, cudaStream_t s);
 
 }  // namespace so2dr_dev

@@ -27,7 +27,7 @@ int k1_max_steps(int dim, int dtype, int kind, int radius) {
     if (kind == KGRAD) return radius == 1 ? 8 : 0;
     if (radius < 1 || radius > 4) return 0;
     if (dtype == 0) return radius == 1 ? 8 : radius == 2 ? 6 : 4;
-    return radius == 1 ? 8 : radius == 2 ? 6 : 2;
+    return radius == 1 ? 8 : radius == 2 ? 6 : radius == 3 ? 2 : 1;
   }
   if (dim == 3) {
     if (kind == KGRAD) return 0;
