@@ -12,26 +12,28 @@
 // taps; gradient: the pinned expression), so results are bit-identical.
 //
 // Design (AN5D-style streaming, B200-first):
-//  * A CTA owns a column strip of NT*V cells (V consecutive cells per thread)
-//    and a segment of output rows; it streams the input rows of the segment
-//    (plus R*S warm-up rows each side) from HBM exactly once. Only the x halo
-//    (R*S columns each side) is recomputed -- the deliberate redundancy of
-//    temporal blocking -- about 2RS/(NT*V) extra work.
-//  * The S time steps are S pipeline stages inside the CTA. Stage u consumes
-//    one row of stage u-1 per iteration and keeps 2R+1 partial accumulators
-//    (one per output row the consumed row contributes to). Because rows arrive
-//    in ascending order, every output point receives its taps in exactly the
-//    canonical (dy, dx) order, so the partial accumulation is bit-exact.
-//  * x neighbours come from warp shuffles; only the two warp-edge lanes go
-//    through shared memory. One __syncthreads per iteration (edge buffers are
-//    double-buffered by iteration parity; each stage consumes what the
-//    previous stage emitted one iteration earlier).
-//  * Input rows are prefetched D rows ahead with 16-byte cp.async (LDGSTS)
-//    into a per-thread shared-memory ring; output rows leave with 16-byte
-//    stores. Each input row is read from HBM once and each output row is
-//    written once: 2*b bytes per cell per launch, i.e. 2b/S per update.
+//  * Every WARP is an independent pipeline: it owns a column strip of 32*V
+//    cells (V consecutive cells per lane) and streams the input rows of its
+//    row segment (plus R*S warm-up rows each side) from HBM exactly once.
+//    x neighbours come from warp shuffles only; the strip's outer R*S columns
+//    are the deliberately recomputed halo of temporal blocking (valid output
+//    32V - 2RS columns). No shared-memory exchange and no __syncthreads in the
+//    main loop, so the S stages of one iteration are independent instruction
+//    streams the scheduler can overlap.
+//  * The S time steps are S pipeline stages. Stage u consumes one row of stage
+//    u-1 per iteration (emitted one iteration earlier) and keeps 2R+1 partial
+//    accumulators (one per output row the consumed row contributes to). Rows
+//    arrive in ascending order, so every output point receives its taps in
+//    exactly the canonical (dy, dx) order: the partial accumulation is
+//    bit-exact.
+//  * Input rows are prefetched kRing-1 rows ahead with cp.async (LDGSTS, 16 B
+//    when aligned) into a per-lane shared-memory ring that only the issuing
+//    lane reads back (no barrier). Each input row is read from HBM once and
+//    each output row written once per launch.
 //  * The main loop is unrolled by 2R+1 so accumulator slot rotation is static
-//    (no local-memory indexing).
+//    (no local-memory indexing), and the steady state (every stage consumes
+//    and emits an interior row, no ring column in the strip) runs a variant
+//    with all range checks compiled away.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -52,9 +54,10 @@ struct K1Args2D {
   int cols;         // padded width
   int y0, y1, x0, x1;
   int iy0, iy1, ix0, ix1;
-  int seg;          // output rows per CTA (y segment)
-  int strip;        // output columns per CTA
-  int xorg;         // thread-column origin of CTA 0 (aligned to VEC)
+  int seg;          // output rows per warp (y segment)
+  int strip;        // output columns per warp
+  int xorg;         // column of lane 0 cell 0 of warp 0 (aligned to VEC)
+  int warps_x;      // warps along x (grid-wide)
   T w[81];          // (2R+1)^2 weights, canonical order
 };
 
@@ -75,16 +78,6 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -94,23 +87,16 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES)
                  : "memory");
 }
-
-// BYTES-wide vector store of consecutive elements
-template <int BYTES>
-__device__ __forceinline__ void store_vec(void* dst, const void* src) {
-  if constexpr (BYTES == 16)
-    *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(src);
-  else if constexpr (BYTES == 8)
-    *reinterpret_cast<float2*>(dst) = *reinterpret_cast<const float2*>(src);
-  else
-    *reinterpret_cast<float*>(dst) = *reinterpret_cast<const float*>(src);
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
-
-// Pipeline depth of the cp.async input ring.
-constexpr int kRing = 4;
 
 template <typename T, int R, int S, int KIND, int V, int NT>
 struct K1Plan2D {
+  // prefetch ring depth (rows per lane; power of two; <= 32 KB of smem)
+  static constexpr int RING = (V * (int)sizeof(T)) <= 16 ? 8 : 4;
   static constexpr int E = 2 * R + 1;
   static constexpr int H = R * S;
   static constexpr int NW = NT / 32;
@@ -126,23 +112,28 @@ template <typename T, int R, int S, int KIND, int V, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
   using P = K1Plan2D<T, R, S, KIND, V, NT>;
   constexpr int E = P::E, H = P::H, NW = P::NW, VEC = P::VEC, CPB = P::CPB;
+  constexpr int kRing = P::RING;
 
   __shared__ __align__(16) T ring[kRing][NT * V];
-  // warp-edge halo values: [parity][producer stage][warp + 1][side][R]
-  __shared__ T edge[2][S][NW + 2][2][R];
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // warp's strip index; surplus warps of the last CTA redo the last strip
+  // without storing (no early exit, so the compiler keeps every shuffle
+  // convergent and emits plain SHFL)
+  const int wx_raw = blockIdx.x * NW + (tid >> 5);
+  const bool live = wx_raw < a.warps_x;
+  const int wx = live ? wx_raw : a.warps_x - 1;
 
-  // ---- CTA geometry -------------------------------------------------------
-  const int tc0 = a.xorg + blockIdx.x * a.strip;  // column of thread 0 cell 0
-  const int OX0 = max(tc0 + H, a.x0);
-  const int OX1 = min(tc0 + H + a.strip, a.x1);
+  // ---- warp geometry ------------------------------------------------------
+  const int wc0 = a.xorg + wx * a.strip;  // column of lane 0 cell 0
+  const int OX0 = max(wc0 + H, a.x0);
+  const int OX1 = min(wc0 + H + a.strip, a.x1);
   const int OY0 = a.y0 + blockIdx.y * a.seg;
   const int OY1 = min(OY0 + a.seg, a.y1);
   const int sy0 = a.base, sy1 = a.base + a.rows;
   const int lo0 = max(OY0 - H, sy0), hi0 = min(OY1 + H, sy1);
   const int n_iter = OY1 - lo0 + S * (R + 1);
-  const int xt = tc0 + tid * V;  // this thread's first column
+  const int xt = wc0 + lane * V;  // this lane's first column
 
   // rows produced by each stage: [lo_u, hi_u)
   int lo[S + 1], hi[S + 1];
@@ -152,29 +143,22 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
     hi[u] = min(OY1 + R * (S - u), sy1);
   }
 
-  // columns needing pass-through (ring / outside the grid)
-  unsigned ringmask = 0;
+  // per-lane column masks: pass-through (ring / outside the grid) and store
+  unsigned ringmask = 0, smask = 0;
 #pragma unroll
   for (int k = 0; k < V; ++k) {
     const int x = xt + k;
     if (x < a.ix0 || x >= a.ix1) ringmask |= 1u << k;
+    if (live && x >= OX0 && x < OX1) smask |= 1u << k;
   }
-  // whole copy vectors inside [0, pitch) are loaded (a thread may straddle
+  // whole copy vectors inside [0, pitch) are loaded (a lane may straddle
   // column 0 when V > VEC, e.g. fp64 with V=4)
-  const bool load_ok = xt + V > 0 && xt < a.pitch;
-  bool store_full = true, store_any = false;
+  unsigned lmask = 0;
 #pragma unroll
-  for (int k = 0; k < V; ++k) {
-    const int x = xt + k;
-    const bool ok = x >= OX0 && x < OX1;
-    store_full = store_full && ok;
-    store_any = store_any || ok;
-  }
-  // CTA-uniform: does any thread own a pass-through column?
-  const bool cta_ring = tc0 < a.ix0 || tc0 + NT * V > a.ix1;
-
-  // zero the edge buffers so out-of-strip halo reads are finite garbage
-  for (int i = tid; i < 2 * S * (NW + 2) * 2 * R; i += NT) (&edge[0][0][0][0][0])[i] = T(0);
+  for (int v = 0; v < V; v += VEC)
+    if (xt + v >= 0 && xt + v < a.pitch) lmask |= 1u << v;
+  // warp-uniform: does any lane own a pass-through column?
+  const bool warp_ring = wc0 < a.ix0 || wc0 + 32 * V > a.ix1;
 
   // carried state
   T cur[S][V];                                // stage 0..S-1 emitted row (own cells)
@@ -185,19 +169,20 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
 #pragma unroll
     for (int k = 0; k < V; ++k) cur[u][k] = T(0);
 
-  // ---- prefetch prologue --------------------------------------------------
-  auto issue = [&](int row, int slot) {
-    if (row >= lo0 && row < hi0 && load_ok) {
-      const T* src = a.in + (int64_t)(row - sy0) * a.pitch + xt;
+  // ---- prefetch (each lane reads back only what it copied: no barrier) ------
+  T* my_ring = &ring[0][tid * V];
+  const T* src_col = a.in + xt;
+  auto issue = [&](int row) {
+    const bool ok = row < hi0;  // rows below lo0 never requested
+    T* dst = my_ring + (row & (kRing - 1)) * (NT * V);
+    const T* src = src_col + (int64_t)(row - sy0) * a.pitch;
 #pragma unroll
-      for (int v = 0; v < V; v += VEC)
-        if (xt + v >= 0) cp_async<CPB>(&ring[slot][tid * V + v], src + v);
-    }
+    for (int v = 0; v < V; v += VEC)
+      if (ok && (lmask & (1u << v))) cp_async<CPB>(dst + v, src + v);
     cp_async_commit();
   };
 #pragma unroll
-  for (int d = 0; d < kRing - 1; ++d) issue(lo0 + d, d);
-  __syncthreads();
+  for (int d = 0; d < kRing - 1; ++d) issue(lo0 + d);
 
   const T* __restrict__ gin = a.in;
   T* __restrict__ gout = a.out;
@@ -210,36 +195,32 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
   };
 
   // One pipeline iteration at compile-time phase PH = it mod E. FAST = steady
-  // state: every stage consumes and emits an interior row and the CTA owns no
-  // pass-through column, so all range checks compile away.
+  // state: every stage consumes and emits an interior row and the strip owns
+  // no pass-through column, so all range checks compile away.
   auto body = [&](auto phase_tag, auto fast_tag, int it) {
     constexpr int PH = decltype(phase_tag)::value;
     constexpr bool FAST = decltype(fast_tag)::value;
-    const int par = it & 1, ppar = par ^ 1;
+    const int row0 = lo0 + it;
 
     // stages in descending order: stage u consumes cur[u-1] (emitted by stage
     // u-1 in the previous iteration) before stage u-1 overwrites it.
 #pragma unroll
     for (int u = S; u >= 1; --u) {
-      const int A = it + lo0 - u - (u - 1) * R;  // row consumed by stage u
-      const int Erow = A - R;                    // row emitted by stage u
+      const int A = row0 - u - (u - 1) * R;  // row consumed by stage u
+      const int Erow = A - R;                // row emitted by stage u
       const bool consume = FAST || (A >= lo[u - 1] && A < hi[u - 1]);
       const bool emit = FAST || (Erow >= lo[u] && Erow < hi[u]);
-      if (!consume && !emit) continue;
 
+      // (shuffles run unconditionally: warp-convergent by construction)
       T seg[V + 2 * R];
-      if (consume) {
 #pragma unroll
-        for (int k = 0; k < V; ++k) seg[R + k] = cur[u - 1][k];
+      for (int k = 0; k < V; ++k) seg[R + k] = cur[u - 1][k];
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
-          T l = __shfl_up_sync(0xffffffffu, cur[u - 1][V - R + j], 1);
-          T rr = __shfl_down_sync(0xffffffffu, cur[u - 1][j], 1);
-          if (lane == 0) l = edge[ppar][u - 1][warp][1][j];
-          if (lane == 31) rr = edge[ppar][u - 1][warp + 2][0][j];
-          seg[j] = l;
-          seg[R + V + j] = rr;
-        }
+      for (int j = 0; j < R; ++j) {
+        // lanes 0 / 31 receive their own values: the strip's outer halo,
+        // finite garbage that never reaches a valid output column
+        seg[j] = __shfl_up_sync(0xffffffffu, cur[u - 1][V - R + j], 1);
+        seg[R + V + j] = __shfl_down_sync(0xffffffffu, cur[u - 1][j], 1);
       }
 
       T outv[V];
@@ -308,48 +289,24 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
         }
         if (u == S) {
           T* dst = gout + (int64_t)(Erow - sy0) * a.pitch + xt;
-          if (store_full) {
 #pragma unroll
-            for (int v = 0; v < V; v += VEC) store_vec<CPB>(dst + v, &outv[v]);
-          } else if (store_any) {
-#pragma unroll
-            for (int k = 0; k < V; ++k)
-              if (xt + k >= OX0 && xt + k < OX1) dst[k] = outv[k];
-          }
+          for (int k = 0; k < V; ++k)
+            if (smask & (1u << k)) dst[k] = outv[k];
         } else {
 #pragma unroll
           for (int k = 0; k < V; ++k) cur[u][k] = outv[k];
-          if (lane == 0) {
-#pragma unroll
-            for (int j = 0; j < R; ++j) edge[par][u][warp + 1][0][j] = outv[j];
-          }
-          if (lane == 31) {
-#pragma unroll
-            for (int j = 0; j < R; ++j) edge[par][u][warp + 1][1][j] = outv[V - R + j];
-          }
         }
       }
     }
 
     // stage 0: row lo0 + it arrives from the cp.async ring
-    {
-      issue(lo0 + it + kRing - 1, (it + kRing - 1) % kRing);
-      cp_async_wait<kRing - 1>();
-      if (FAST || lo0 + it < hi0) {
-        const int slot = it % kRing;
+    issue(row0 + kRing - 1);
+    cp_async_wait<kRing - 1>();
+    if (FAST || row0 < hi0) {
+      const T* src = my_ring + (row0 & (kRing - 1)) * (NT * V);
 #pragma unroll
-        for (int k = 0; k < V; ++k) cur[0][k] = ring[slot][tid * V + k];
-        if (lane == 0) {
-#pragma unroll
-          for (int j = 0; j < R; ++j) edge[par][0][warp + 1][0][j] = cur[0][j];
-        }
-        if (lane == 31) {
-#pragma unroll
-          for (int j = 0; j < R; ++j) edge[par][0][warp + 1][1][j] = cur[0][V - R + j];
-        }
-      }
+      for (int k = 0; k < V; ++k) cur[0][k] = src[k];
     }
-    __syncthreads();
   };
 
   // ---- steady-state window [f_lo, f_hi): every stage consumes a stored row
@@ -363,7 +320,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
     f_lo = max(f_lo, max(lo[u], a.iy0) + R - c);
     f_hi = min(f_hi, min(hi[u], a.iy1) + R - c);
   }
-  if (cta_ring) f_hi = f_lo;
+  if (warp_ring) f_hi = f_lo;
 
   int it = 0;
   auto run_general = [&](int stop) {

@@ -55,11 +55,14 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   for (int i = 0; i < 81; ++i) a.w[i] = T(0);
   if (L.w)
     for (int i = 0; i < E * E; ++i) a.w[i] = static_cast<T>(L.w[i]);
-  a.strip = ((NT * V - 2 * H) / VEC) * VEC;
+  // one warp = one independent strip of 32*V columns, 2H of them halo
+  a.strip = ((32 * V - 2 * H) / VEC) * VEC;
   if (a.strip <= 0) return cudaErrorInvalidValue;
   a.xorg = floor_div(L.x0 - H, VEC) * VEC;
   const int width = L.x1 - (a.xorg + H);
-  const int nx = std::max(1, (width + a.strip - 1) / a.strip);
+  a.warps_x = std::max(1, (width + a.strip - 1) / a.strip);
+  constexpr int NW = NT / 32;
+  const int nx = (a.warps_x + NW - 1) / NW;
   const int height = L.y1 - L.y0;
   // y segments: enough CTAs for ~4 waves at MINB CTAs per SM, but keep each
   // segment long against its R*S warm-up + S*(R+1) pipeline fill.
