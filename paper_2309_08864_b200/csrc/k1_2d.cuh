@@ -57,7 +57,9 @@ struct K1Args2D {
   int seg;          // output rows per warp (y segment)
   int strip;        // output columns per warp
   int xorg;         // column of lane 0 cell 0 of warp 0 (aligned to VEC)
-  int warps_x;      // warps along x (grid-wide)
+  int warps_x;      // strips along x
+  int nseg;         // row segments; work items = warps_x * nseg
+  unsigned* counter;  // work-item counter (zeroed before the launch)
   T w[81];          // (2R+1)^2 weights, canonical order
 };
 
@@ -77,6 +79,31 @@ __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, 
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+// Packed fp32 pair helpers for FFMA2 (PTX fma.rn.f32x2, new in sm_100).
+// The packing movs are register-pair renames the compiler folds into the
+// FFMA2 operand swizzles (.F32x2.HI_LO / .LO_HI).
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(uint64_t r, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+// {lo, hi} = {w * a0 + c.lo, w * a1 + c.hi}, each rounded once (RN)
+__device__ __forceinline__ uint64_t fma2(float w, float a0, float a1, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pack2(w, w)), "l"(pack2(a0, a1)), "l"(c));
+  return d;
+}
+
+// {lo, hi} = {w * a.lo + c.lo, w * a.hi + c.hi} on an already packed pair
+__device__ __forceinline__ uint64_t fma2p(float w, uint64_t a, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pack2(w, w)), "l"(a), "l"(c));
+  return d;
+}
 
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
@@ -108,27 +135,22 @@ struct K1Plan2D {
   static constexpr int NGR = (KIND == KGRAD) ? S : 0;
 };
 
-template <typename T, int R, int S, int KIND, int V, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
+// One work item = (strip wx, row segment sg) processed by one warp; `ring` is
+// the calling CTA's shared ring (each lane uses its own slots only).
+template <typename T, int R, int S, int KIND, int V, int NT>
+__device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
+                                        T (&ring)[K1Plan2D<T, R, S, KIND, V, NT>::RING][NT * V]) {
   using P = K1Plan2D<T, R, S, KIND, V, NT>;
-  constexpr int E = P::E, H = P::H, NW = P::NW, VEC = P::VEC, CPB = P::CPB;
+  constexpr int E = P::E, H = P::H, VEC = P::VEC, CPB = P::CPB;
   constexpr int kRing = P::RING;
-
-  __shared__ __align__(16) T ring[kRing][NT * V];
-
   const int tid = threadIdx.x, lane = tid & 31;
-  // warp's strip index; surplus warps of the last CTA redo the last strip
-  // without storing (no early exit, so the compiler keeps every shuffle
-  // convergent and emits plain SHFL)
-  const int wx_raw = blockIdx.x * NW + (tid >> 5);
-  const bool live = wx_raw < a.warps_x;
-  const int wx = live ? wx_raw : a.warps_x - 1;
+  constexpr bool live = true;
 
   // ---- warp geometry ------------------------------------------------------
   const int wc0 = a.xorg + wx * a.strip;  // column of lane 0 cell 0
   const int OX0 = max(wc0 + H, a.x0);
   const int OX1 = min(wc0 + H + a.strip, a.x1);
-  const int OY0 = a.y0 + blockIdx.y * a.seg;
+  const int OY0 = a.y0 + sg * a.seg;
   const int OY1 = min(OY0 + a.seg, a.y1);
   const int sy0 = a.base, sy1 = a.base + a.rows;
   const int lo0 = max(OY0 - H, sy0), hi0 = min(OY1 + H, sy1);
@@ -249,6 +271,32 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
           for (int m = 0; m < E; ++m) {
             const int dy = m - R;                 // A contributes at dy to row A-dy
             const int sl = (PH - m + 2 * E) % E;  // slot of output row A+R-m
+            if constexpr (sizeof(T) == 4 && V % 2 == 0) {
+              // fp32: two cells per FFMA2 (fma.rn.f32x2, sm_100a); each half is
+              // an IEEE fma with round-to-nearest, so the chain is bit-identical
+              // to the scalar __fmaf_rn chain. Cells are paired (k, k+V/2), not
+              // (k, k+1): then the operand pair for every dx, (s[k+dx],
+              // s[k+V/2+dx]), is the same register pair the previous stage
+              // emitted, except the 2R pairs that take a shuffled halo value --
+              // so almost no register moves are needed to form operands.
+              constexpr int HV = V / 2;
+#pragma unroll
+              for (int k = 0; k < HV; ++k) {
+                uint64_t x = (m == 0) ? 0ull : pack2(acc[u - 1][sl][k], acc[u - 1][sl][k + HV]);
+                if constexpr (KIND == KBOX) {
+#pragma unroll
+                  for (int dx = -R; dx <= R; ++dx)
+                    x = fma2(a.w[(dy + R) * E + dx + R], seg[R + k + dx], seg[R + k + HV + dx], x);
+                } else if (dy != 0) {
+                  x = fma2(a.w[(dy + R) * E + R], seg[R + k], seg[R + k + HV], x);
+                } else {
+#pragma unroll
+                  for (int dx = -R; dx <= R; ++dx)
+                    x = fma2(a.w[R * E + dx + R], seg[R + k + dx], seg[R + k + HV + dx], x);
+                }
+                unpack2(x, acc[u - 1][sl][k], acc[u - 1][sl][k + HV]);
+              }
+            } else {
 #pragma unroll
             for (int k = 0; k < V; ++k) {
               T x = (m == 0) ? T(0) : acc[u - 1][sl][k];
@@ -266,6 +314,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
                 }
               }
               acc[u - 1][sl][k] = x;
+            }
             }
           }
         }
@@ -343,6 +392,251 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
   }
   run_general(n_iter);
   cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// Packed fp32 variant for box / star: identical pipeline, but every carried
+// value lives in 64-bit register pairs holding cells (k, k + V/2) of the
+// lane, and every multiply-add is an FFMA2 (fma.rn.f32x2). With this pairing
+// the operand pair of every tap, (s[k+dx], s[k+V/2+dx]), is either a pair the
+// previous stage emitted as-is or one of the 2R pairs formed with a shuffled
+// halo value, so the FMA pipe spends its cycles on FFMA2, not on register
+// moves (each FMA-pipe instruction costs 2 issue cycles per SMSP; FFMA2 does
+// 64 fmas in them, a scalar FFMA 32). Each half is an IEEE round-to-nearest
+// fma: results are bit-identical to the scalar chain.
+template <int R, int S, int KIND, int V, int NT>
+__device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int sg,
+                                           float (&ring)[K1Plan2D<float, R, S, KIND, V, NT>::RING][NT * V]) {
+  using T = float;
+  using P = K1Plan2D<T, R, S, KIND, V, NT>;
+  constexpr int E = P::E, H = P::H, VEC = P::VEC, CPB = P::CPB;
+  constexpr int kRing = P::RING;
+  constexpr int HV = V / 2;
+  constexpr int NP = HV + 2 * R;  // operand pairs per consumed row
+  static_assert(V % 2 == 0 && KIND != KGRAD, "packed path: box/star, even V");
+  const int tid = threadIdx.x, lane = tid & 31;
+  constexpr bool live = true;
+  const int wc0 = a.xorg + wx * a.strip;
+  const int OX0 = max(wc0 + H, a.x0);
+  const int OX1 = min(wc0 + H + a.strip, a.x1);
+  const int OY0 = a.y0 + sg * a.seg;
+  const int OY1 = min(OY0 + a.seg, a.y1);
+  const int sy0 = a.base, sy1 = a.base + a.rows;
+  const int lo0 = max(OY0 - H, sy0), hi0 = min(OY1 + H, sy1);
+  const int n_iter = OY1 - lo0 + S * (R + 1);
+  const int xt = wc0 + lane * V;
+
+  int lo[S + 1], hi[S + 1];
+#pragma unroll
+  for (int u = 0; u <= S; ++u) {
+    lo[u] = max(OY0 - R * (S - u), sy0);
+    hi[u] = min(OY1 + R * (S - u), sy1);
+  }
+  unsigned ringmask = 0, smask = 0;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int x = xt + k;
+    if (x < a.ix0 || x >= a.ix1) ringmask |= 1u << k;
+    if (live && x >= OX0 && x < OX1) smask |= 1u << k;
+  }
+  unsigned lmask = 0;
+#pragma unroll
+  for (int v = 0; v < V; v += VEC)
+    if (xt + v >= 0 && xt + v < a.pitch) lmask |= 1u << v;
+  const bool warp_ring = wc0 < a.ix0 || wc0 + 32 * V > a.ix1;
+
+  // cell k of a packed row: pair k % HV, half k / HV
+  auto cell = [](const uint64_t (&p)[HV], int k) -> float {
+    float lo, hi;
+    unpack2(p[k % HV], lo, hi);
+    return k < HV ? lo : hi;
+  };
+
+  // Stage u's emitted row is never copied: it stays in its accumulator slot,
+  // which stage u+1 reads in the next iteration before stage u re-initialises
+  // it (stages run in descending order). Only stage 0 has its own row.
+  uint64_t cp0[HV];        // stage 0 (loaded) row, packed
+  uint64_t ap[S][E][HV];   // partial accumulators, packed
+#pragma unroll
+  for (int k = 0; k < HV; ++k) cp0[k] = 0ull;
+#pragma unroll
+  for (int u = 0; u < S; ++u)
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+#pragma unroll
+      for (int k = 0; k < HV; ++k) ap[u][e][k] = 0ull;
+
+  T* my_ring = &ring[0][tid * V];
+  const T* src_col = a.in + xt;
+  auto issue = [&](int row) {
+    const bool ok = row < hi0;
+    T* dst = my_ring + (row & (kRing - 1)) * (NT * V);
+    const T* src = src_col + (int64_t)(row - sy0) * a.pitch;
+#pragma unroll
+    for (int v = 0; v < V; v += VEC)
+      if (ok && (lmask & (1u << v))) cp_async<CPB>(dst + v, src + v);
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int d = 0; d < kRing - 1; ++d) issue(lo0 + d);
+
+  auto passthru = [&](int row, int k) -> T {
+    const int x = xt + k;
+    if (x < 0 || x >= a.cols) return T(0);
+    return __ldg(a.in + (int64_t)(row - sy0) * a.pitch + x);
+  };
+
+  auto body = [&](auto phase_tag, auto fast_tag, int it) {
+    constexpr int PH = decltype(phase_tag)::value;
+    constexpr bool FAST = decltype(fast_tag)::value;
+    const int row0 = lo0 + it;
+#pragma unroll
+    for (int u = S; u >= 1; --u) {
+      const int A = row0 - u - (u - 1) * R;
+      const int Erow = A - R;
+      const bool consume = FAST || (A >= lo[u - 1] && A < hi[u - 1]);
+      const bool emit = FAST || (Erow >= lo[u] && Erow < hi[u]);
+
+      // the consumed row: stage u-1's emission of the previous iteration
+      uint64_t in[HV];
+#pragma unroll
+      for (int k = 0; k < HV; ++k) in[k] = (u == 1) ? cp0[k] : ap[u >= 2 ? u - 2 : 0][PH][k];
+      // halo values (lanes 0/31 get their own: strip-edge garbage, never output)
+      float hl[R], hr[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        hl[j] = __shfl_up_sync(0xffffffffu, cell(in, V - R + j), 1);
+        hr[j] = __shfl_down_sync(0xffffffffu, cell(in, j), 1);
+      }
+      // s_i: i < R halo-left, R <= i < R+V own cell i-R, else halo-right
+      auto sval = [&](int i) -> float {
+        if (i < R) return hl[i];
+        if (i < R + V) return cell(in, i - R);
+        return hr[i - R - V];
+      };
+      uint64_t op[NP];  // op[j] = (s_j, s_{j+HV})
+#pragma unroll
+      for (int j = 0; j < NP; ++j) op[j] = (j >= R && j < R + HV) ? in[j - R] : pack2(sval(j), sval(j + HV));
+
+      if (consume) {
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+          const int dy = m - R;
+          const int sl = (PH - m + 2 * E) % E;
+#pragma unroll
+          for (int k = 0; k < HV; ++k) {
+            uint64_t x = (m == 0) ? 0ull : ap[u - 1][sl][k];
+            if constexpr (KIND == KBOX) {
+#pragma unroll
+              for (int dx = -R; dx <= R; ++dx) x = fma2p(a.w[(dy + R) * E + dx + R], op[R + k + dx], x);
+            } else if (dy != 0) {
+              x = fma2p(a.w[(dy + R) * E + R], op[R + k], x);
+            } else {
+#pragma unroll
+              for (int dx = -R; dx <= R; ++dx) x = fma2p(a.w[R * E + dx + R], op[R + k + dx], x);
+            }
+            ap[u - 1][sl][k] = x;
+          }
+        }
+      }
+      if (emit) {
+        constexpr int se = (PH - 2 * R + 2 * E) % E;
+        uint64_t outp[HV];
+#pragma unroll
+        for (int k = 0; k < HV; ++k) outp[k] = ap[u - 1][se][k];
+        if constexpr (!FAST) {
+          const bool ring_row = Erow < a.iy0 || Erow >= a.iy1;
+          if (ring_row || ringmask) {
+            float v[V];
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+              v[k] = cell(outp, k);
+              if (ring_row || (ringmask & (1u << k))) v[k] = passthru(Erow, k);
+            }
+#pragma unroll
+            for (int k = 0; k < HV; ++k) ap[u - 1][se][k] = outp[k] = pack2(v[k], v[k + HV]);
+          }
+        }
+        if (u == S) {
+          T* dst = a.out + (int64_t)(Erow - sy0) * a.pitch + xt;
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            if (smask & (1u << k)) dst[k] = cell(outp, k);
+        }
+      }
+    }
+    issue(row0 + kRing - 1);
+    cp_async_wait<kRing - 1>();
+    if (FAST || row0 < hi0) {
+      const T* src = my_ring + (row0 & (kRing - 1)) * (NT * V);
+#pragma unroll
+      for (int k = 0; k < HV; ++k) cp0[k] = pack2(src[k], src[k + HV]);
+    }
+  };
+
+  int f_lo = 0, f_hi = hi0 - lo0;
+#pragma unroll
+  for (int u = 1; u <= S; ++u) {
+    const int c = lo0 - u - (u - 1) * R;
+    f_lo = max(f_lo, lo[u - 1] - c);
+    f_hi = min(f_hi, hi[u - 1] - c);
+    f_lo = max(f_lo, max(lo[u], a.iy0) + R - c);
+    f_hi = min(f_hi, min(hi[u], a.iy1) + R - c);
+  }
+  if (warp_ring) f_hi = f_lo;
+
+  int it = 0;
+  auto run_general = [&](int stop) {
+    while (it < stop) {
+      [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
+        ((it < stop ? (body(std::integral_constant<int, Ps>{}, std::false_type{}, it), ++it, void())
+                    : void()),
+         ...);
+      }(std::make_integer_sequence<int, E>{});
+    }
+  };
+  const int fl = (f_lo + E - 1) / E * E;
+  if (f_hi - fl >= E) {
+    run_general(fl);
+    while (it + E <= f_hi) {
+      [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
+        ((body(std::integral_constant<int, Ps>{}, std::true_type{}, it), ++it), ...);
+      }(std::make_integer_sequence<int, E>{});
+    }
+  }
+  run_general(n_iter);
+  cp_async_wait<0>();
+}
+
+// Persistent warps with dynamic work distribution: every warp of a
+// one-wave grid fetches (strip, segment) items from an atomic counter, so the
+// SMs stay busy until the last item (no partial last wave).
+template <typename T, int R, int S, int KIND, int V, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
+  __shared__ __align__(16) T ring[K1Plan2D<T, R, S, KIND, V, NT>::RING][NT * V];
+  const int lane = threadIdx.x & 31;
+  const int total = a.warps_x * a.nseg;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = static_cast<int>(atomicAdd(a.counter, 1u));
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= total) break;
+    k1_item<T, R, S, KIND, V, NT>(a, item % a.warps_x, item / a.warps_x, ring);
+  }
+}
+
+template <int R, int S, int KIND, int V, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k1_stencil2d_pk(const K1Args2D<float> a) {
+  __shared__ __align__(16) float ring[K1Plan2D<float, R, S, KIND, V, NT>::RING][NT * V];
+  const int lane = threadIdx.x & 31;
+  const int total = a.warps_x * a.nseg;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = static_cast<int>(atomicAdd(a.counter, 1u));
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= total) break;
+    k1_item_pk<R, S, KIND, V, NT>(a, item % a.warps_x, item / a.warps_x, ring);
+  }
 }
 
 }  // namespace so2dr_dev

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <utility>
 
 #include "k1_2d.cuh"
@@ -21,7 +22,9 @@ constexpr int v2d(int R) {
 }
 template <typename T>
 constexpr int maxs2d(int R) {
-  return sizeof(T) == 4 ? (R == 1 ? 8 : R == 2 ? 6 : 4) : (R == 1 ? 8 : R == 2 ? 6 : R == 3 ? 2 : 1);
+  // (2R+1)^2 taps x S stages x 2R+1 unrolled phases grows fast: larger radii
+  // fuse fewer steps per launch (the engine splits longer calls)
+  return sizeof(T) == 4 ? (R == 1 ? 8 : R == 2 ? 4 : R == 3 ? 2 : 1) : (R == 1 ? 8 : R == 2 ? 4 : 1);
 }
 
 inline int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
@@ -62,19 +65,35 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   const int width = L.x1 - (a.xorg + H);
   a.warps_x = std::max(1, (width + a.strip - 1) / a.strip);
   constexpr int NW = NT / 32;
-  const int nx = (a.warps_x + NW - 1) / NW;
   const int height = L.y1 - L.y0;
-  // y segments: enough CTAs for ~4 waves at MINB CTAs per SM, but keep each
-  // segment long against its R*S warm-up + S*(R+1) pipeline fill.
+  // One wave of persistent CTAs; warps pull (strip, segment) items from a
+  // counter. Segments: ~8 items per resident warp for load balance, but each
+  // at least 6x its warm-up (R*S rows + S*(R+1) pipeline fill) long.
+  constexpr bool packed = std::is_same_v<T, float> && KIND != KGRAD && V % 2 == 0;
+  auto kern = [] {
+    if constexpr (packed)
+      return k1_stencil2d_pk<R, S, KIND, V, NT, MINB>;
+    else
+      return k1_stencil2d<T, R, S, KIND, V, NT, MINB>;
+  }();
+  static int occ = 0;
+  if (occ == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0) != cudaSuccess || occ < 1)
+      occ = 1;
+  }
   const int sms = device_sm_count();
+  const int resident_warps = sms * occ * NW;
   const int min_seg = std::max(48, 6 * (H + S * (R + 1)));
-  const int max_ny = std::max(1, height / min_seg);
-  int ny = std::max(1, (4 * MINB * sms + nx - 1) / nx);
-  ny = std::min(ny, max_ny);
-  a.seg = (height + ny - 1) / ny;
-  ny = (height + a.seg - 1) / a.seg;
-  dim3 grid(nx, ny);
-  k1_stencil2d<T, R, S, KIND, V, NT, MINB><<<grid, NT, 0, stream>>>(a);
+  const int max_ns = std::max(1, height / min_seg);
+  int ns = std::max(1, (8 * resident_warps + a.warps_x - 1) / a.warps_x);
+  ns = std::min(ns, max_ns);
+  a.seg = (height + ns - 1) / ns;
+  a.nseg = (height + a.seg - 1) / a.seg;
+  a.counter = k1_next_counter(stream);
+  if (!a.counter) return cudaErrorUnknown;
+  const int items = a.warps_x * a.nseg;
+  const int ctas = std::max(1, std::min(sms * occ, (items + NW - 1) / NW));
+  kern<<<ctas, NT, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

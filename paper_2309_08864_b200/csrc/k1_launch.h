@@ -48,4 +48,7 @@ cudaError_t launch_k1_3d_f64(const K1Launch& L, cudaStream_t stream);
 
 int device_sm_count();
 
+// Zeroed work counter for one persistent K1 launch on `stream`.
+unsigned* k1_next_counter(cudaStream_t stream);
+
 }  // namespace so2dr_dev

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 
 #include "k1_launch.h"
@@ -26,8 +27,9 @@ int k1_max_steps(int dim, int dtype, int kind, int radius) {
   if (dim == 2) {
     if (kind == KGRAD) return radius == 1 ? 8 : 0;
     if (radius < 1 || radius > 4) return 0;
-    if (dtype == 0) return radius == 1 ? 8 : radius == 2 ? 6 : 4;
-    return radius == 1 ? 8 : radius == 2 ? 6 : radius == 3 ? 2 : 1;
+    // must match maxs2d() in k1_2d_impl.cuh
+    if (dtype == 0) return radius == 1 ? 8 : radius == 2 ? 4 : radius == 3 ? 2 : 1;
+    return radius == 1 ? 8 : radius == 2 ? 4 : 1;
   }
   if (dim == 3) {
     if (kind == KGRAD) return 0;
@@ -97,4 +99,28 @@ cudaError_t launch_init(int dtype, void* out, int64_t pitch, int p, int dim, int
   return cudaGetLastError();
 }
 
+}  // namespace so2dr_dev
+
+// ---- work counters for the persistent K1 kernels ---------------------------
+// A ring of device counters per device; each launch takes the next slot and
+// zeroes it on its own stream first. A slot is reused only 65536 launches
+// later, long after the earlier launch finished.
+namespace so2dr_dev {
+constexpr unsigned kCounters = 65536;
+__device__ unsigned g_k1_counters[kCounters];
+
+unsigned* k1_next_counter(cudaStream_t stream) {
+  static unsigned* base[64] = {};
+  static std::atomic<unsigned> next{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!base[dev]) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_k1_counters) != cudaSuccess) return nullptr;
+    base[dev] = static_cast<unsigned*>(p);
+  }
+  unsigned* slot = base[dev] + (next.fetch_add(1) % kCounters);
+  if (cudaMemsetAsync(slot, 0, sizeof(unsigned), stream) != cudaSuccess) return nullptr;
+  return slot;
+}
 }  // namespace so2dr_dev
