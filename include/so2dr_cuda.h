@@ -123,7 +123,8 @@ typedef struct {
 typedef struct {
   int32_t round, chunk, stage, reserved;
   uint64_t bytes, updates;
-  double ms; /* measured stage duration (CUDA events), 0 when not timed */
+  double ms;    /* measured stage duration (CUDA events), 0 when not timed */
+  double t0_ms; /* stage start relative to the run's first enqueue (when timed) */
 } so2dr_diag_row;
 
 typedef struct so2dr_ctx so2dr_ctx;

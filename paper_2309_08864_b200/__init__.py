@@ -104,7 +104,7 @@ class _Timing(ctypes.Structure):
 class _Diag(ctypes.Structure):
     _fields_ = [("round", ctypes.c_int32), ("chunk", ctypes.c_int32), ("stage", ctypes.c_int32),
                 ("reserved", ctypes.c_int32), ("bytes", ctypes.c_uint64), ("updates", ctypes.c_uint64),
-                ("ms", ctypes.c_double)]
+                ("ms", ctypes.c_double), ("t0_ms", ctypes.c_double)]
 
 
 PEER_BLOB_BYTES = 512
@@ -401,7 +401,7 @@ class Engine:
             for i in range(min(n.value, cap)):
                 d = rows[i]
                 dl.append({"round": d.round, "chunk": d.chunk, "stage": STAGES[d.stage],
-                           "bytes": d.bytes, "updates": d.updates, "ms": d.ms})
+                           "bytes": d.bytes, "updates": d.updates, "ms": d.ms, "t0_ms": d.t0_ms})
         return RunReport(mode, config, {f: getattr(led, f) for f in LEDGER_FIELDS},
                          {f: getattr(tim, f) for f, _ in TIMING_FIELDS}, dl)
 

@@ -960,9 +960,11 @@ void run(so2dr_ctx* ctx, RunRequest& q, RunResponse& out) {
   tm.kernel_launches = rec.kernel.size();
   tm.kernel_alg_bytes = rec.alg_bytes;
   for (size_t i = 0; i < rec.stage.size(); ++i) {
-    float k = 0.f;
+    float k = 0.f, t0 = 0.f;
     SO2DR_CK(cudaEventElapsedTime(&k, rec.stage[i].first, rec.stage[i].second));
+    SO2DR_CK(cudaEventElapsedTime(&t0, ev_start, rec.stage[i].first));
     out.diag[rec.stage_idx[i]].ms = k;
+    out.diag[rec.stage_idx[i]].t0_ms = t0;
   }
   tm.h2d_bytes = acc.L.htod;
   tm.d2h_bytes = acc.L.dtoh;

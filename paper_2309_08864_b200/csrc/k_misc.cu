@@ -34,8 +34,9 @@ int k1_max_steps(int dim, int dtype, int kind, int radius) {
   if (dim == 3) {
     if (kind == KGRAD) return 0;
     if (radius < 1 || radius > 2) return 0;
-    if (dtype == 0) return radius == 1 ? 8 : 4;
-    return radius == 1 ? 4 : 2;
+    // must match maxs3d() in k1_3d.cu
+    if (dtype == 0) return radius == 1 ? 4 : 2;
+    return radius == 1 ? 2 : 1;
   }
   return 0;
 }

@@ -21,7 +21,9 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,extra", [(2, {}), (4, {}), (2, {"SLAB_DIM": "3", "SLAB_KIND": "star"}),
+@pytest.mark.parametrize("world,extra", [(2, {}), (4, {}),
+                                         (2, {"SLAB_DIM": "3", "SLAB_KIND": "star", "SLAB_STB": "2",
+                                              "SLAB_KON": "2", "SLAB_N": "5"}),
                                          (2, {"SLAB_DTYPE": "f64", "SLAB_KIND": "star"}),
                                          (2, {"SLAB_STB": "6", "SLAB_KON": "4", "SLAB_N": "13"})])
 def test_slab_engine_shared_device(world, extra):

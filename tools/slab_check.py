@@ -40,7 +40,7 @@ def main():
     eng = so2dr.Engine(dev)
     lo, hi = so2dr.slab_rows(cfg, rank, world, dim)
     full = o.init_grid(sz, r, 42, dim, dtype)
-    slab = np.ascontiguousarray(full[lo:hi])
+    slab = full[lo:hi].copy()  # a view would let the engine advance `full` itself
     blob = eng.slab_prepare(spec, cfg, dtype, rank, world)
     blobs = [None] * world
     dist.all_gather_object(blobs, blob)
@@ -65,7 +65,9 @@ def main():
         ok_htod = htod == (sz + 2 * r) * unit * rounds  # no halo byte crossed PCIe twice
         print(f"SLAB world={world} dim={dim} {np.dtype(dtype).name} diffs={len(bad)} htod_ok={ok_htod}", flush=True)
         if len(bad) or not ok_htod:
-            print("first diffs", bad[:5], flush=True)
+            rows = np.unique(bad[:, 0])
+            print("first diffs", bad[:5], "rows with diffs", rows[:20], "...", rows[-5:], "n rows", len(rows),
+                  "slabs", [(a, b) for a, b, _, _ in parts], flush=True)
             sys.exit(1)
     dist.barrier()
     eng.close()
