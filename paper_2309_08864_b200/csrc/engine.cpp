@@ -87,8 +87,26 @@ CUresult cuStreamWriteValue32_rt(CUstream s, CUdeviceptr a, cuuint32_t v, unsign
 void* Pool::get(const std::string& id, uint64_t bytes) {
   bytes = std::max<uint64_t>(bytes, 256);
   auto it = blk_.find(id);
-  if (it != blk_.end() && it->second.bytes >= bytes) return it->second.p;
-  const uint64_t others = used() - (it != blk_.end() ? it->second.bytes : 0);
+  if (it != blk_.end() && it->second.bytes >= bytes) {
+    it->second.gen = gen_;
+    return it->second.p;
+  }
+  uint64_t others = used() - (it != blk_.end() ? it->second.bytes : 0);
+  if (others + bytes > budget) {
+    // drop cached blocks the current run has not asked for
+    cudaDeviceSynchronize();
+    for (auto jt = blk_.begin(); jt != blk_.end();) {
+      // never the slab exchange block: a neighbour holds an IPC mapping of it
+      if (jt->second.gen != gen_ && jt->first != id && jt->first.rfind("slab.", 0) != 0) {
+        cudaFree(jt->second.p);
+        jt = blk_.erase(jt);
+      } else {
+        ++jt;
+      }
+    }
+    it = blk_.find(id);
+    others = used() - (it != blk_.end() ? it->second.bytes : 0);
+  }
   if (others + bytes > budget)
     throw OutOfDeviceMemoryError("hbm:" + id, bytes, others, budget);
   if (it != blk_.end()) {
@@ -102,7 +120,7 @@ void* Pool::get(const std::string& id, uint64_t bytes) {
     throw OutOfDeviceMemoryError("hbm:" + id, bytes, others, budget);
   }
   SO2DR_CK(e);
-  blk_[id] = Blk{p, bytes};
+  blk_[id] = Blk{p, bytes, gen_};
   return p;
 }
 
@@ -164,7 +182,12 @@ Geo make_geo(int dim, int sz, int r, int dtype) {
   g.r = r;
   g.p = sz + 2 * r;
   g.elem = dtype == SO2DR_F64 ? 8 : 4;
-  g.pitch = (static_cast<int64_t>(g.p) + 31) / 32 * 32;
+  // Dense rows (pitch = padded width, same as the host grid): every chunk
+  // transfer is then ONE contiguous cudaMemcpyAsync. Pitched 2D copies run at
+  // only ~42 GB/s per direction when H2D and D2H overlap vs ~50 GB/s for
+  // contiguous ones (tools/cu/copy2d_bench.cu, measured on this pool's B200).
+  // K1 copies rows with cp.async pieces that divide the pitch (16/8/4 bytes).
+  g.pitch = g.p;
   g.unit_rows = dim == 3 ? g.p : 1;
   return g;
 }
@@ -373,6 +396,11 @@ uint64_t device_footprint(const so2dr::RunConfig& cfg, const Geo& g, int n_strm)
 static void copy_units(const Geo& g, void* dst, int64_t dst_pitch, const void* src,
                        int64_t src_pitch, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
+  if (dst_pitch == g.p && src_pitch == g.p) {  // dense on both sides: one contiguous copy
+    SO2DR_CK(cudaMemcpyAsync(dst, src, static_cast<size_t>(n * g.unit_rows * g.p * g.elem),
+                             cudaMemcpyDefault, s));
+    return;
+  }
   SO2DR_CK(cudaMemcpy2DAsync(dst, dst_pitch * g.elem, src, src_pitch * g.elem,
                              static_cast<size_t>(g.p) * g.elem,
                              static_cast<size_t>(n * g.unit_rows), cudaMemcpyDefault, s));
@@ -900,6 +928,7 @@ void run(so2dr_ctx* ctx, RunRequest& q, RunResponse& out) {
 
   SO2DR_CK(cudaSetDevice(ctx->device));
   ctx->events.recycle();
+  ctx->pool.begin_run();
   out.diag.clear();
 
   // host grid: pin it for the duration of the call if it is large pageable memory

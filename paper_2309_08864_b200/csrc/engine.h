@@ -22,6 +22,9 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 class Pool {
  public:
   uint64_t budget = 0;
+  // Blocks requested since the last begin_run() are "live"; older ones are
+  // freed on demand when a request would exceed the budget.
+  void begin_run() { ++gen_; }
   void* get(const std::string& id, uint64_t bytes);
   uint64_t used() const;
   void release_all();
@@ -31,8 +34,10 @@ class Pool {
   struct Blk {
     void* p = nullptr;
     uint64_t bytes = 0;
+    uint64_t gen = 0;
   };
   std::map<std::string, Blk> blk_;
+  uint64_t gen_ = 1;
 };
 
 // Recycled CUDA events (timing and non-timing kinds).

@@ -59,6 +59,7 @@ struct K1Args2D {
   int xorg;         // column of lane 0 cell 0 of warp 0 (aligned to VEC)
   int warps_x;      // strips along x
   int nseg;         // row segments; work items = warps_x * nseg
+  int cpb;          // cp.async piece bytes (16/8/4): largest dividing the pitch
   unsigned* counter;  // work-item counter (zeroed before the launch)
   T w[81];          // (2R+1)^2 weights, canonical order
 };
@@ -118,6 +119,30 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Copy the VEC consecutive elements at column x of one row, global -> shared,
+// with cp.async pieces of `cpb` bytes (16, 8 or 4): the largest size that
+// divides the row pitch in bytes, so a dense (unpadded) row layout works at
+// any alignment. Pieces outside [0, pitch) are skipped (no piece ever reads
+// across the row end).
+template <typename T, int VEC>
+__device__ __forceinline__ void issue_vec(T* dst, const T* src, int cpb, int x, int64_t pitch) {
+  constexpr int VB = VEC * (int)sizeof(T);
+  auto piece = [&](auto bytes_tag) {
+    constexpr int B = decltype(bytes_tag)::value;
+    constexpr int PE = B / (int)sizeof(T) > 0 ? B / (int)sizeof(T) : 1;
+#pragma unroll
+    for (int b = 0, e = 0; b < VB; b += B, e += PE)
+      if (x + e >= 0 && x + e + PE <= pitch)
+        cp_async<B>(reinterpret_cast<char*>(dst) + b, reinterpret_cast<const char*>(src) + b);
+  };
+  if (VB >= 16 && cpb >= 16)
+    piece(std::integral_constant<int, 16>{});
+  else if (VB >= 8 && cpb >= 8)
+    piece(std::integral_constant<int, 8>{});
+  else
+    piece(std::integral_constant<int, (sizeof(T) >= 8 ? 8 : 4)>{});
 }
 
 template <typename T, int R, int S, int KIND, int V, int NT>
@@ -200,7 +225,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
     const T* src = src_col + (int64_t)(row - sy0) * a.pitch;
 #pragma unroll
     for (int v = 0; v < V; v += VEC)
-      if (ok && (lmask & (1u << v))) cp_async<CPB>(dst + v, src + v);
+      if (ok) issue_vec<T, VEC>(dst + v, src + v, a.cpb, xt + v, a.pitch);
     cp_async_commit();
   };
 #pragma unroll
@@ -474,7 +499,7 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
     const T* src = src_col + (int64_t)(row - sy0) * a.pitch;
 #pragma unroll
     for (int v = 0; v < V; v += VEC)
-      if (ok && (lmask & (1u << v))) cp_async<CPB>(dst + v, src + v);
+      if (ok) issue_vec<T, VEC>(dst + v, src + v, a.cpb, xt + v, a.pitch);
     cp_async_commit();
   };
 #pragma unroll

@@ -58,6 +58,10 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   for (int i = 0; i < 81; ++i) a.w[i] = T(0);
   if (L.w)
     for (int i = 0; i < E * E; ++i) a.w[i] = static_cast<T>(L.w[i]);
+  {
+    const int64_t pb = L.pitch * static_cast<int64_t>(sizeof(T));
+    a.cpb = pb % 16 == 0 ? 16 : pb % 8 == 0 ? 8 : 4;
+  }
   // one warp = one independent strip of 32*V columns, 2H of them halo
   a.strip = ((32 * V - 2 * H) / VEC) * VEC;
   if (a.strip <= 0) return cudaErrorInvalidValue;

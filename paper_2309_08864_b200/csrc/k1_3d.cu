@@ -47,6 +47,7 @@ struct K1Args3D {
   int seg;               // output planes per CTA
   int tile_x, tile_y;    // valid output cells per CTA along x / y
   int xorg, yorg;        // origin of CTA (0,0)'s thread cell (aligned)
+  int cpb;               // cp.async piece bytes (largest of 16/8/4 dividing the pitch)
   T w[125];              // (2R+1)^3 canonical weights
 };
 
@@ -121,8 +122,9 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
       const bool rok = ok && y >= 0 && y < a.p;
 #pragma unroll
       for (int v = 0; v < V; v += VEC)
-        if (rok && xt + v >= 0 && xt + v < a.pitch)
-          cp_async<CPB>(&ring[plane & (RING - 1)][j][tid * V + v], src + (int64_t)y * a.pitch + xt + v);
+        if (rok)
+          issue_vec<T, VEC>(&ring[plane & (RING - 1)][j][tid * V + v], src + (int64_t)y * a.pitch + xt + v,
+                            a.cpb, xt + v, a.pitch);
     }
     cp_async_commit();
   };
@@ -286,6 +288,10 @@ cudaError_t launch3(const K1Launch& L, cudaStream_t stream) {
   a.in = static_cast<const T*>(L.in);
   a.out = static_cast<T*>(L.out);
   a.pitch = L.pitch;
+  {
+    const int64_t pb = L.pitch * static_cast<int64_t>(sizeof(T));
+    a.cpb = pb % 16 == 0 ? 16 : pb % 8 == 0 ? 8 : 4;
+  }
   a.p = L.cols;
   a.plane_stride = static_cast<int64_t>(L.plane_rows) * L.pitch;
   a.base = L.base;
