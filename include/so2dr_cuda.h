@@ -143,6 +143,12 @@ int so2dr_abi_version(void);
 /* Number of visible CUDA devices (0 when none; never fails). */
 int so2dr_device_count(void);
 
+/* Pinned host allocation for grids (cudaHostAlloc, portable). Preferred over
+ * registering malloc'd memory: on this pool's B200 hosts, 4 KiB-page
+ * registered memory sustains only ~43 GB/s per direction when H2D and D2H
+ * overlap, cudaHostAlloc / huge-page memory ~50 GB/s (tools/cu/pin_bench.cu). */
+so2dr_status so2dr_host_alloc(so2dr_ctx* ctx, size_t bytes, void** out);
+so2dr_status so2dr_host_free(so2dr_ctx* ctx, void* p);
 /* Pin a caller-owned host range (cudaHostRegister); idempotent per range. */
 so2dr_status so2dr_host_register(so2dr_ctx* ctx, void* base, size_t bytes);
 so2dr_status so2dr_host_unregister(so2dr_ctx* ctx, void* base);

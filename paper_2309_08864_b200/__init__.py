@@ -116,6 +116,7 @@ EXPORTS = (
     "so2dr_abi_version", "so2dr_device_count", "so2dr_ctx_create", "so2dr_ctx_destroy",
     "so2dr_ctx_set_profiling", "so2dr_last_error", "so2dr_last_constraint",
     "so2dr_last_allocation_id", "so2dr_host_register", "so2dr_host_unregister", "so2dr_run",
+    "so2dr_host_alloc", "so2dr_host_free",
     "so2dr_slab_rows", "so2dr_slab_prepare", "so2dr_slab_connect", "so2dr_slab_run",
     "so2dr_fused_kernel", "so2dr_apply_step", "so2dr_run_reference", "so2dr_init_grid",
     "so2dr_init_rows", "so2dr_grid_checksum", "so2dr_arena_bytes", "so2dr_device_bytes",
@@ -143,6 +144,8 @@ def lib():
         getattr(L, f).argtypes = [vp]
         getattr(L, f).restype = ctypes.c_char_p
     L.so2dr_host_register.argtypes = [vp, vp, sz]
+    L.so2dr_host_alloc.argtypes = [vp, sz, P(vp)]
+    L.so2dr_host_free.argtypes = [vp, vp]
     L.so2dr_host_unregister.argtypes = [vp, vp]
     L.so2dr_run.argtypes = [vp, i32, P(_Stencil), P(_Cfg), P(_KPlan), P(_HW), P(_Hooks), i32, vp,
                             P(_Ledger), P(_Timing), P(_Diag), sz, P(sz)]
@@ -364,6 +367,20 @@ class Engine:
 
     def set_profiling(self, on: bool):
         self._ck(lib().so2dr_ctx_set_profiling(self._h, 1 if on else 0))
+
+    def host_array(self, shape, dtype=np.float32) -> np.ndarray:
+        """numpy array over pinned memory from so2dr_host_alloc (cudaHostAlloc); freed
+        when the array is garbage-collected."""
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = ctypes.c_void_p()
+        self._ck(lib().so2dr_host_alloc(self._h, nbytes, ctypes.byref(p)))
+        buf = (ctypes.c_char * nbytes).from_address(p.value)
+        arr = np.frombuffer(buf, dtype=dtype).reshape(shape)
+        h, L = self._h, lib()
+        import weakref
+
+        weakref.finalize(buf, L.so2dr_host_free, h, p.value)
+        return arr
 
     def host_register(self, arr):
         self._ck(lib().so2dr_host_register(self._h, _ptr(arr), arr.nbytes if isinstance(arr, np.ndarray)

@@ -156,6 +156,27 @@ const char* so2dr_last_allocation_id(const so2dr_ctx* ctx) {
   return ctx ? ctx->alloc_id.c_str() : tl_alloc.c_str();
 }
 
+so2dr_status so2dr_host_alloc(so2dr_ctx* ctx, size_t bytes, void** out) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    if (!out || !bytes) throw so2dr::ContractError("host_alloc: bad arguments");
+    SO2DR_CK(cudaSetDevice(ctx->device));
+    const cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocPortable);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      throw so2dr::OutOfDeviceMemoryError("host:pinned", bytes, 0, 0);
+    }
+    SO2DR_CK(e);
+  });
+}
+
+so2dr_status so2dr_host_free(so2dr_ctx* ctx, void* p) {
+  return guard(ctx, [&] {
+    need_ctx(ctx);
+    if (p) SO2DR_CK(cudaFreeHost(p));
+  });
+}
+
 so2dr_status so2dr_host_register(so2dr_ctx* ctx, void* base, size_t bytes) {
   return guard(ctx, [&] {
     need_ctx(ctx);

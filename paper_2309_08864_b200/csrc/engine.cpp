@@ -1,16 +1,17 @@
-// engine.cu -- the B200 SO2DR out-of-core scheduler.
+// engine.cpp -- the B200 SO2DR out-of-core scheduler.
 //
 // Replaces the reference executor proj/src/engine.cpp:200-449
 // (run_out_of_core, so2dr_chunk, resreu_chunk, run_incore). Where the
 // reference runs N_strm std::thread workers that memcpy between host vectors
 // and synchronise through Gates (engine.cpp:75-120), this engine enqueues the
-// whole run from ONE host thread onto N_strm CUDA streams; every
-// happens-before edge of the reference becomes a cudaEvent wait:
+// whole run from ONE host thread onto CUDA streams; every happens-before edge
+// of the reference becomes a stream order or a cudaEvent wait. so2dr mode:
 //
-//   stream(i % N_strm):  [wait D2H_{t-1}(i+1)] H2D(transfer_i) -> ring rows ->
-//                        [wait PUB(i-1)] slot -> shared_in, record SLOTFREE ->
-//                        [wait SLOTFREE(slot)] shared_out -> slot, record PUB(i) ->
-//                        K1 x calls_in_round -> D2H(core_i), record D2H(i)
+//   H2D stream:     [wait pair (i mod N_strm) drained] [wait D2H_{t-1}(i+1)]
+//                   H2D(transfer_i) -> record H2D(i)
+//   compute stream: [wait H2D(i)] ring rows -> slot(i-1) -> shared_in ->
+//                   shared_out -> slot(i) -> K1 x calls_in_round -> record CMP(i)
+//   D2H stream:     [wait CMP(i)] D2H(core_i) -> record D2H(i) (frees pair)
 //
 // The host never blocks until the final synchronize, so H2D, kernels and
 // D2H of different chunks overlap on the two copy engines and the SMs.
@@ -309,10 +310,10 @@ so2dr::KernelStats tile_stats(int r, int steps, int tile, Rect region, Rect inte
 
 // ----------------------------------------------------------- K1 dispatch --
 
-void k1_call(so2dr_ctx* ctx, cudaStream_t s, const Geo& g, const StencilDev& st, const void* rd,
+bool k1_call(so2dr_ctx* ctx, cudaStream_t s, const Geo& g, const StencilDev& st, const void* rd,
              void* wr, int base, int rows, int y0, int y1, int x0, int x1, int steps,
-             int scratch_slot, const int32_t* interior) {
-  if (y1 <= y0 || x1 <= x0 || steps < 1) return;
+             int scratch_slot, const int32_t* interior, bool pingpong) {
+  if (y1 <= y0 || x1 <= x0 || steps < 1) return false;
   so2dr_dev::K1Launch L;
   L.dim = g.dim;
   L.dtype = g.elem == 8 ? 1 : 0;
@@ -356,16 +357,23 @@ void k1_call(so2dr_ctx* ctx, cudaStream_t s, const Geo& g, const StencilDev& st,
   };
   if (steps <= m) {
     launch(rd, wr, y0, y1, x0, x1, steps);
-    return;
+    return false;
   }
   // Split into ceil(steps/m) launches. Intermediate launches produce the
-  // trapezoid rows still needed (region grown by r*remaining steps) into two
-  // scratch fields; only the last launch writes the destination, so cells of
-  // `wr` outside the region stay untouched (reference semantics).
-  const uint64_t field_bytes = static_cast<uint64_t>(rows) * g.dev_unit_elems() * g.elem;
-  void* scr[2] = {ctx->pool.get("scratch" + std::to_string(scratch_slot) + ".a", field_bytes),
-                  ctx->pool.get("scratch" + std::to_string(scratch_slot) + ".b", field_bytes)};
+  // trapezoid rows still needed (region grown by r*remaining steps).
+  //  * pingpong (engine chunks, whose read buffer is dead after the call):
+  //    pieces alternate rd -> wr -> rd ...; returns true when the result
+  //    landed in `rd` (even number of pieces). No extra memory.
+  //  * otherwise (fused_kernel semantics: `rd` and the cells of `wr` outside
+  //    the region stay untouched): intermediates go to two scratch fields and
+  //    only the last launch writes `wr`.
   const int pieces = (steps + m - 1) / m;
+  void* scr[2] = {nullptr, nullptr};
+  if (!pingpong) {
+    const uint64_t field_bytes = static_cast<uint64_t>(rows) * g.dev_unit_elems() * g.elem;
+    scr[0] = ctx->pool.get("scratch" + std::to_string(scratch_slot) + ".a", field_bytes);
+    scr[1] = ctx->pool.get("scratch" + std::to_string(scratch_slot) + ".b", field_bytes);
+  }
   int remaining = steps;
   const void* in = rd;
   for (int k = 0; k < pieces; ++k) {
@@ -374,10 +382,11 @@ void k1_call(so2dr_ctx* ctx, cudaStream_t s, const Geo& g, const StencilDev& st,
     const int grow = R * remaining;
     const int ly0 = std::max(base, y0 - grow), ly1 = std::min(base + rows, y1 + grow);
     const int lx0 = std::max(0, x0 - grow), lx1 = std::min(g.dim == 3 ? g.p : g.p, x1 + grow);
-    void* out = (k == pieces - 1) ? wr : scr[k & 1];
+    void* out = pingpong ? ((k & 1) ? const_cast<void*>(rd) : wr) : ((k == pieces - 1) ? wr : scr[k & 1]);
     launch(in, out, ly0, ly1, lx0, lx1, sub);
     in = out;
   }
+  return pingpong && (pieces % 2 == 0);
 }
 
 uint64_t device_footprint(const so2dr::RunConfig& cfg, const Geo& g, int n_strm) {
@@ -544,17 +553,22 @@ struct Recorder {
 
 // One K1 call over rows [y0, y1) x all columns, bracketed by timing events on
 // its own stream (the bench's per-launch kernel time).
-void k1_timed(RunCtx& rc, Recorder& rec, cudaStream_t s, const StencilDev& st, const Field& f,
+// returns true when the result landed in buffer `rd` (split call, pingpong)
+bool k1_timed(RunCtx& rc, Recorder& rec, cudaStream_t s, const StencilDev& st, const Field& f,
               int rows, int rd, int y0, int y1, int steps, int slot) {
   cudaEvent_t a = rc.ctx->events.timing_event(), b = rc.ctx->events.timing_event();
   SO2DR_CK(cudaEventRecord(a, s));
-  k1_call(rc.ctx, s, rc.g, st, f.buf[rd], f.buf[rd ^ 1], f.base, rows, y0, y1, 0, rc.g.p, steps,
-          slot, nullptr);
+  // SO2DR_DIAG_NO_K1=1: transfer-only diagnostic runs (results are wrong)
+  static const bool no_k1 = std::getenv("SO2DR_DIAG_NO_K1") != nullptr;
+  const bool in_rd = no_k1 ? false
+                           : k1_call(rc.ctx, s, rc.g, st, f.buf[rd], f.buf[rd ^ 1], f.base, rows,
+                                     y0, y1, 0, rc.g.p, steps, slot, nullptr, /*pingpong=*/true);
   SO2DR_CK(cudaEventRecord(b, s));
   rec.kernel.push_back({a, b});
   const int lo = std::max(f.base, y0 - st.radius * steps);
   const int hi = std::min(f.base + rows, y1 + st.radius * steps);
   rec.alg_bytes += static_cast<uint64_t>((hi - lo) + (y1 - y0)) * rc.g.unit_bytes();
+  return in_rd;
 }
 
 cudaEvent_t record_sync(so2dr_ctx* ctx, cudaStream_t s) {
@@ -570,6 +584,13 @@ void wait(cudaStream_t s, cudaEvent_t e) {
 CUdeviceptr dptr(const void* p) { return reinterpret_cast<CUdeviceptr>(p); }
 
 // ---- so2dr: round-based streaming with region sharing (engine.cpp:200-318)
+//
+// Three dedicated streams form the pipeline: H2D (copy engine 0) -> compute
+// (region sharing + K1 calls, in chunk order) -> D2H (copy engine 1). Chunk i
+// lives in buffer pair (i mod N_strm); the H2D of chunk i waits only for that
+// pair to be drained by the D2H of chunk i - N_strm, so the two copy
+// directions stream back to back while kernels run (the reference's N_strm
+// workers each serialised H2D -> kernel -> D2H of one chunk).
 void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc& acc,
                Recorder& rec) {
   so2dr_ctx* ctx = rc.ctx;
@@ -582,11 +603,8 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
   const int dl = d / world;
   const int cb = rank * dl, ce = cb + dl;  // chunks owned by this rank
   const bool has_lo = rank > 0, has_hi = rank < world - 1;
-  const Rect interior{r, r + cfg.sz, 0, 0};
   const int64_t cols = g.host_unit_elems();
-  Rect inter = interior;
-  inter.x0 = g.dim == 3 ? 0 : r;
-  inter.x1 = g.dim == 3 ? static_cast<int>(cols) : g.p - r;
+  const Rect inter{r, r + cfg.sz, g.dim == 3 ? 0 : r, g.dim == 3 ? static_cast<int>(cols) : g.p - r};
 
   int max_work = 0;
   for (int i = cb; i < ce; ++i) max_work = std::max(max_work, lay.chunks[i].working.height());
@@ -606,9 +624,16 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
   char* band_hi = nullptr;
   if (has_lo) band_lo = static_cast<char*>(ctx->pool.get("band.lo", h * unit));
   if (has_hi) band_hi = static_cast<char*>(ctx->pool.get("band.hi", h * unit));
-  cudaStream_t aux_lo = ctx->stream(ns), aux_hi = ctx->stream(ns + 1);
+  cudaStream_t s_h2d = ctx->stream(0), s_cmp = ctx->stream(1), s_d2h = ctx->stream(2);
+  cudaStream_t aux_lo = ctx->stream(3), aux_hi = ctx->stream(4);
 
-  std::vector<cudaEvent_t> ev_pub(d, nullptr), ev_d2h(d, nullptr), ev_free(slots, nullptr);
+  std::vector<cudaEvent_t> ev_h2d(d, nullptr), ev_cmp(d, nullptr), ev_d2h(d, nullptr);
+  std::vector<cudaEvent_t> ev_pair_free(ns, nullptr);  // last D2H out of buffer pair k
+  std::vector<cudaEvent_t> d2h_hist;                   // D2H events in issue order
+  static const int lead = [] {
+    const char* e = std::getenv("SO2DR_H2D_LEAD");
+    return e ? std::atoi(e) : 0;
+  }();
   cudaEvent_t ev_band_lo = nullptr, ev_band_hi = nullptr, ev_lo_used = nullptr,
               ev_hi_used = nullptr;
 
@@ -647,85 +672,86 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
 
     for (int i = cb; i < ce; ++i) {
       const so2dr::ChunkIntervals& ci = lay.chunks[i];
-      const int sidx = (i - cb) % ns;
-      cudaStream_t s = ctx->stream(sidx);
-      Field& f = F[sidx];
+      const int pk = (i - cb) % ns;
+      Field& f = F[pk];
       f.base = ci.working.lo;
 
+      // ---- H2D stream: transfer rows into buf0 of pair pk --------------------
+      wait(s_h2d, ev_pair_free[pk]);  // drained by the D2H of chunk i - N_strm
+      // flow control: keep H2D at most `lead` chunks ahead of D2H so both
+      // directions stay busy together (the link favours H2D when both run)
+      if (lead > 0 && static_cast<int>(d2h_hist.size()) >= lead)
+        wait(s_h2d, d2h_hist[d2h_hist.size() - lead]);
       // host write-after-read across rounds: our transfer rows overlap the
       // core of chunk i+1, which that chunk wrote back last round
-      if (t > 0 && i + 1 < ce && (i + 1 - cb) % ns != sidx) wait(s, ev_d2h[i + 1]);
-
-      // H2D of the transfer rows (the slab edge bands are already staged)
+      if (t > 0 && i + 1 < ce) wait(s_h2d, ev_d2h[i + 1]);
       RowInterval tr = ci.transfer;
       if (i == cb && has_lo) tr.lo = std::max(tr.lo, lay.fence[cb] + h);
       if (i == ce - 1 && has_hi) tr.hi = lay.fence[ce] - h;
-      cudaEvent_t sb = rc.stage_begin(s);
-      rc.h2d(f, 0, tr, s);
+      cudaEvent_t sb = rc.stage_begin(s_h2d);
+      rc.h2d(f, 0, tr, s_h2d);
       acc.L.htod += rc.bytes(tr.height());
-      uint64_t htod_b = rc.bytes(tr.height());
+      rc.stage_end(sb, s_h2d, t, i, Stage::htod, rc.bytes(tr.height()), 0, rec.stage,
+                   rec.stage_idx);
+      ev_h2d[i] = record_sync(ctx, s_h2d);
+
+      // ---- compute stream: ring rows, region sharing, K1 calls ----------------
+      wait(s_cmp, ev_h2d[i]);
       // constant ring rows seed the second buffer (engine.cpp:398-401)
-      if (i == 0) rc.d2d(rc.dev_at(f, 1, 0), rc.dev_at(f, 0, 0), r, s);
-      if (i == d - 1) rc.d2d(rc.dev_at(f, 1, r + cfg.sz), rc.dev_at(f, 0, r + cfg.sz), r, s);
+      if (i == 0) rc.d2d(rc.dev_at(f, 1, 0), rc.dev_at(f, 0, 0), r, s_cmp);
+      if (i == d - 1) rc.d2d(rc.dev_at(f, 1, r + cfg.sz), rc.dev_at(f, 0, r + cfg.sz), r, s_cmp);
       if (i == ce - 1 && has_hi) {
         // our upper edge band, then the neighbour's rows above it
-        wait(s, ev_band_hi);
-        rc.d2d(rc.dev_at(f, 0, lay.fence[ce] - h), band_hi, h, s);
-        ev_hi_used = record_sync(ctx, s);
-        check_cu(cuStreamWaitValue32(s, dptr(&sl.flags[1]), epoch + 1, CU_STREAM_WAIT_VALUE_GEQ),
+        wait(s_cmp, ev_band_hi);
+        rc.d2d(rc.dev_at(f, 0, lay.fence[ce] - h), band_hi, h, s_cmp);
+        ev_hi_used = record_sync(ctx, s_cmp);
+        check_cu(cuStreamWaitValue32(s_cmp, dptr(&sl.flags[1]), epoch + 1, CU_STREAM_WAIT_VALUE_GEQ),
                  "wait data hi");
-        rc.d2d(rc.dev_at(f, 0, lay.fence[ce]), static_cast<char*>(sl.recv_hi), h, s);
-        check_cu(cuStreamWriteValue32(s, dptr(sl.upper.ack), epoch + 1, 0), "ack hi");
+        rc.d2d(rc.dev_at(f, 0, lay.fence[ce]), static_cast<char*>(sl.recv_hi), h, s_cmp);
+        check_cu(cuStreamWriteValue32(s_cmp, dptr(sl.upper.ack), epoch + 1, 0), "ack hi");
       }
-      rc.stage_end(sb, s, t, i, Stage::htod, htod_b, 0, rec.stage, rec.stage_idx);
-
-      // region sharing: consume the slab of boundary i-1 (engine.cpp:277-284)
+      // region sharing: consume the slab of boundary i-1 (engine.cpp:277-284);
+      // chunk order on one stream is the reference's publish-before-consume
       if (i > cb) {
-        sb = rc.stage_begin(s);
-        wait(s, ev_pub[i - 1]);
-        const int j = (i - 1) % slots;
-        rc.d2d(rc.dev_at(f, 0, ci.shared_in.lo), slot[j], 2 * h, s);
-        ev_free[j] = record_sync(ctx, s);
+        sb = rc.stage_begin(s_cmp);
+        rc.d2d(rc.dev_at(f, 0, ci.shared_in.lo), slot[(i - 1) % slots], 2 * h, s_cmp);
         acc.L.ondevice += rc.bytes(2 * h);
-        rc.stage_end(sb, s, t, i, Stage::share_read, rc.bytes(2 * h), 0, rec.stage,
+        rc.stage_end(sb, s_cmp, t, i, Stage::share_read, rc.bytes(2 * h), 0, rec.stage,
                      rec.stage_idx);
       } else if (has_lo) {
-        sb = rc.stage_begin(s);
-        check_cu(cuStreamWaitValue32(s, dptr(&sl.flags[0]), epoch + 1, CU_STREAM_WAIT_VALUE_GEQ),
+        sb = rc.stage_begin(s_cmp);
+        check_cu(cuStreamWaitValue32(s_cmp, dptr(&sl.flags[0]), epoch + 1, CU_STREAM_WAIT_VALUE_GEQ),
                  "wait data lo");
-        rc.d2d(rc.dev_at(f, 0, lay.fence[cb] - h), static_cast<char*>(sl.recv_lo), h, s);
-        check_cu(cuStreamWriteValue32(s, dptr(sl.lower.ack), epoch + 1, 0), "ack lo");
-        wait(s, ev_band_lo);
-        rc.d2d(rc.dev_at(f, 0, lay.fence[cb]), band_lo, h, s);
-        ev_lo_used = record_sync(ctx, s);
-        rc.stage_end(sb, s, t, i, Stage::share_read, rc.bytes(2 * h), 0, rec.stage,
+        rc.d2d(rc.dev_at(f, 0, lay.fence[cb] - h), static_cast<char*>(sl.recv_lo), h, s_cmp);
+        check_cu(cuStreamWriteValue32(s_cmp, dptr(sl.lower.ack), epoch + 1, 0), "ack lo");
+        wait(s_cmp, ev_band_lo);
+        rc.d2d(rc.dev_at(f, 0, lay.fence[cb]), band_lo, h, s_cmp);
+        ev_lo_used = record_sync(ctx, s_cmp);
+        rc.stage_end(sb, s_cmp, t, i, Stage::share_read, rc.bytes(2 * h), 0, rec.stage,
                      rec.stage_idx);
       }
       // publish the slab of boundary i before any kernel rewrites buf0
       // (engine.cpp:285-293; SURVEY 7 hard part 5)
       if (i < ce - 1) {
-        sb = rc.stage_begin(s);
-        const int j = i % slots;
-        wait(s, ev_free[j]);
+        sb = rc.stage_begin(s_cmp);
+        char* sj = slot[i % slots];
         if (q.hooks.corrupt_share && q.hooks.boundary == i)
-          SO2DR_CK(cudaMemsetAsync(slot[j], 0, 2ull * h * unit, s));
+          SO2DR_CK(cudaMemsetAsync(sj, 0, 2ull * h * unit, s_cmp));
         else
-          rc.d2d(slot[j], rc.dev_at(f, 0, ci.shared_out.lo), 2 * h, s);
-        ev_pub[i] = record_sync(ctx, s);
+          rc.d2d(sj, rc.dev_at(f, 0, ci.shared_out.lo), 2 * h, s_cmp);
         acc.L.ondevice += rc.bytes(2 * h);
-        rc.stage_end(sb, s, t, i, Stage::share_write, rc.bytes(2 * h), 0, rec.stage,
+        rc.stage_end(sb, s_cmp, t, i, Stage::share_write, rc.bytes(2 * h), 0, rec.stage,
                      rec.stage_idx);
       }
-
       // K1 calls over shrinking trapezoids (engine.cpp:295-310)
-      sb = rc.stage_begin(s);
+      sb = rc.stage_begin(s_cmp);
       int rd = 0, done = 0;
       uint64_t kb = 0, ku = 0;
       for (int c = 0; c < calls; ++c) {
         const int sc = rp.steps_in_call(t, c);
         done += sc;
         const RowInterval area = so2dr::compute_area(lay, i, done, k_eff);
-        k1_timed(rc, rec, s, q.st, f, ci.working.height(), rd, area.lo, area.hi, sc, sidx);
+        const bool stay = k1_timed(rc, rec, s_cmp, q.st, f, ci.working.height(), rd, area.lo, area.hi, sc, pk);
         const so2dr::KernelStats ks = tile_stats(
             r, sc, q.kp.tile, Rect{area.lo, area.hi, 0, static_cast<int>(cols)}, inter,
             Rect{ci.core.lo, ci.core.hi, 0, static_cast<int>(cols)}, ci.working.lo,
@@ -733,16 +759,20 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
         acc.add_kernel(ks);
         kb += ks.scratch_load + ks.scratch_store;
         ku += ks.updates;
-        rd ^= 1;
+        if (!stay) rd ^= 1;
       }
-      rc.stage_end(sb, s, t, i, Stage::kernel, kb, ku, rec.stage, rec.stage_idx);
+      rc.stage_end(sb, s_cmp, t, i, Stage::kernel, kb, ku, rec.stage, rec.stage_idx);
+      ev_cmp[i] = record_sync(ctx, s_cmp);
 
-      // D2H of the core rows (engine.cpp:312-317)
-      sb = rc.stage_begin(s);
-      rc.d2h(f, rd, ci.core, s);
-      ev_d2h[i] = record_sync(ctx, s);
+      // ---- D2H stream: core rows back to the host (engine.cpp:312-317) --------
+      wait(s_d2h, ev_cmp[i]);
+      sb = rc.stage_begin(s_d2h);
+      rc.d2h(f, rd, ci.core, s_d2h);
+      ev_d2h[i] = record_sync(ctx, s_d2h);
+      ev_pair_free[pk] = ev_d2h[i];
+      d2h_hist.push_back(ev_d2h[i]);
       acc.L.dtoh += rc.bytes(ci.core.height());
-      rc.stage_end(sb, s, t, i, Stage::dtoh, rc.bytes(ci.core.height()), 0, rec.stage,
+      rc.stage_end(sb, s_d2h, t, i, Stage::dtoh, rc.bytes(ci.core.height()), 0, rec.stage,
                    rec.stage_idx);
     }
     acc.L.rounds += 1;
@@ -778,12 +808,12 @@ void run_incore(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Ac
   const Rect region{r, r + cfg.sz, 0, static_cast<int>(cols)};
   while (done < cfg.n) {
     const int sc = std::min(q.kp.k_on, cfg.n - done);
-    k1_timed(rc, rec, s, q.st, f, p, rd, r, r + cfg.sz, sc, 0);
+    const bool stay = k1_timed(rc, rec, s, q.st, f, p, rd, r, r + cfg.sz, sc, 0);
     const so2dr::KernelStats ks = tile_stats(r, sc, q.kp.tile, region, inter, region, 0, p, cols);
     acc.add_kernel(ks);
     kb += ks.scratch_load + ks.scratch_store;
     ku += ks.updates;
-    rd ^= 1;
+    if (!stay) rd ^= 1;
     done += sc;
   }
   rc.stage_end(sb, s, 0, 0, Stage::kernel, kb, ku, rec.stage, rec.stage_idx);
@@ -961,17 +991,18 @@ void run(so2dr_ctx* ctx, RunRequest& q, RunResponse& out) {
   Acc acc;
   Recorder rec;
   cudaStream_t s0 = ctx->stream(0);
-  for (int k = 1; k < ns + 2; ++k) ctx->stream(k);
+  const int nstreams = std::max(ns + 2, 5);  // so2dr: h2d, compute, d2h, 2 slab-edge streams
+  for (int k = 1; k < nstreams; ++k) ctx->stream(k);
   cudaEvent_t ev_start = ctx->events.timing_event(), ev_end = ctx->events.timing_event();
   SO2DR_CK(cudaEventRecord(ev_start, s0));
-  for (int k = 1; k < ns + 2; ++k) wait(ctx->stream(k), ev_start);
+  for (int k = 1; k < nstreams; ++k) wait(ctx->stream(k), ev_start);
 
   switch (q.mode) {
     case SO2DR_MODE_SO2DR: run_so2dr(rc, q, cfg, acc, rec); break;
     case SO2DR_MODE_INCORE: run_incore(rc, q, cfg, acc, rec); break;
     case SO2DR_MODE_RESREU: run_resreu(rc, q, cfg, acc, rec); break;
   }
-  for (int k = 1; k < ns + 2; ++k) wait(s0, record_sync(ctx, ctx->stream(k)));
+  for (int k = 1; k < nstreams; ++k) wait(s0, record_sync(ctx, ctx->stream(k)));
   SO2DR_CK(cudaEventRecord(ev_end, s0));
   SO2DR_CK(cudaEventSynchronize(ev_end));
   SO2DR_CK(cudaGetLastError());

@@ -160,9 +160,11 @@ void slab_prepare(so2dr_ctx* ctx, const StencilDev& st, const so2dr_run_config& 
 void slab_connect(so2dr_ctx* ctx, const uint8_t* lower, const uint8_t* upper);
 
 // kernel launch (device-resident field) with step splitting
-void k1_call(so2dr_ctx* ctx, cudaStream_t s, const Geo& g, const StencilDev& st, const void* rd,
+// Returns true when the result landed in `rd` (only with pingpong = true and
+// a call split into an even number of launches).
+bool k1_call(so2dr_ctx* ctx, cudaStream_t s, const Geo& g, const StencilDev& st, const void* rd,
              void* wr, int base, int rows, int y0, int y1, int x0, int x1, int steps,
-             int scratch_slot, const int32_t* interior = nullptr);
+             int scratch_slot, const int32_t* interior = nullptr, bool pingpong = false);
 
 // reference kernel ledger accounting (proj/src/kernels.cpp:48-138) in closed form
 so2dr::KernelStats tile_stats(int r, int steps, int tile, so2dr::Rect region,

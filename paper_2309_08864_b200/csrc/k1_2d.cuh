@@ -122,27 +122,43 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // Copy the VEC consecutive elements at column x of one row, global -> shared,
-// with cp.async pieces of `cpb` bytes (16, 8 or 4): the largest size that
-// divides the row pitch in bytes, so a dense (unpadded) row layout works at
-// any alignment. Pieces outside [0, pitch) are skipped (no piece ever reads
-// across the row end).
+// with cp.async pieces of `cpb` bytes (16, 8 or 4; the caller picks the
+// largest the row's start address allows -- dense rows of odd-multiple
+// pitches alternate 16- and 8-byte alignment). A piece that would cross the
+// row end falls back to per-element copies of its in-row part; elements
+// outside [0, pitch) are skipped.
 template <typename T, int VEC>
 __device__ __forceinline__ void issue_vec(T* dst, const T* src, int cpb, int x, int64_t pitch) {
   constexpr int VB = VEC * (int)sizeof(T);
+  constexpr int EB = sizeof(T) >= 8 ? 8 : 4;  // one element
   auto piece = [&](auto bytes_tag) {
     constexpr int B = decltype(bytes_tag)::value;
     constexpr int PE = B / (int)sizeof(T) > 0 ? B / (int)sizeof(T) : 1;
 #pragma unroll
-    for (int b = 0, e = 0; b < VB; b += B, e += PE)
-      if (x + e >= 0 && x + e + PE <= pitch)
+    for (int b = 0, e = 0; b < VB; b += B, e += PE) {
+      if (x + e >= 0 && x + e + PE <= pitch) {
         cp_async<B>(reinterpret_cast<char*>(dst) + b, reinterpret_cast<const char*>(src) + b);
+      } else if constexpr (PE > 1) {
+#pragma unroll
+        for (int j = 0; j < PE; ++j)
+          if (x + e + j >= 0 && x + e + j < pitch)
+            cp_async<EB>(reinterpret_cast<char*>(dst) + b + j * EB,
+                         reinterpret_cast<const char*>(src) + b + j * EB);
+      }
+    }
   };
   if (VB >= 16 && cpb >= 16)
     piece(std::integral_constant<int, 16>{});
   else if (VB >= 8 && cpb >= 8)
     piece(std::integral_constant<int, 8>{});
   else
-    piece(std::integral_constant<int, (sizeof(T) >= 8 ? 8 : 4)>{});
+    piece(std::integral_constant<int, EB>{});
+}
+
+// Largest cp.async piece (16/8/4 bytes) a row starting at `row_start` allows.
+__device__ __forceinline__ int row_cpb(const void* row_start) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(row_start);
+  return (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : 4;
 }
 
 template <typename T, int R, int S, int KIND, int V, int NT>
@@ -223,9 +239,10 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
     const bool ok = row < hi0;  // rows below lo0 never requested
     T* dst = my_ring + (row & (kRing - 1)) * (NT * V);
     const T* src = src_col + (int64_t)(row - sy0) * a.pitch;
+    const int cpb = row_cpb(a.in + (int64_t)(row - sy0) * a.pitch);  // warp-uniform
 #pragma unroll
     for (int v = 0; v < V; v += VEC)
-      if (ok) issue_vec<T, VEC>(dst + v, src + v, a.cpb, xt + v, a.pitch);
+      if (ok) issue_vec<T, VEC>(dst + v, src + v, cpb, xt + v, a.pitch);
     cp_async_commit();
   };
 #pragma unroll
@@ -497,9 +514,10 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
     const bool ok = row < hi0;
     T* dst = my_ring + (row & (kRing - 1)) * (NT * V);
     const T* src = src_col + (int64_t)(row - sy0) * a.pitch;
+    const int cpb = row_cpb(a.in + (int64_t)(row - sy0) * a.pitch);  // warp-uniform
 #pragma unroll
     for (int v = 0; v < V; v += VEC)
-      if (ok) issue_vec<T, VEC>(dst + v, src + v, a.cpb, xt + v, a.pitch);
+      if (ok) issue_vec<T, VEC>(dst + v, src + v, cpb, xt + v, a.pitch);
     cp_async_commit();
   };
 #pragma unroll

@@ -11,8 +11,7 @@ import paper_2309_08864_b200 as so2dr  # noqa: E402
 
 sz = 92160
 eng = so2dr.Engine(0, 16 << 30)
-host = np.empty((sz + 2, sz + 2), np.float32)
-eng.host_register(host)
+host = eng.host_array((sz + 2, sz + 2), np.float32)
 eng.init_grid(sz, 1, 42, out=host)
 spec = so2dr.StencilSpec.box(1)
 for d, ns, k in itertools.product((16, 32, 48, 64), (3, 4, 6), (4, 8)):

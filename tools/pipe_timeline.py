@@ -25,8 +25,7 @@ def union(iv):
 
 sz = 92160
 eng = so2dr.Engine(0, 16 << 30)
-host = np.empty((sz + 2, sz + 2), np.float32)
-eng.host_register(host)
+host = eng.host_array((sz + 2, sz + 2), np.float32)
 eng.init_grid(sz, 1, 42, out=host)
 spec = so2dr.StencilSpec.box(1)
 for d, ns in ((16, 3), (64, 3), (64, 4), (96, 3)):
