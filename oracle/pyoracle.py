@@ -51,6 +51,8 @@ def lib():
             getattr(L, f"orc_init_{t}").argtypes = [vp, i, i, i, u64]
             getattr(L, f"orc_step_{t}").argtypes = [vp, vp, i, i, ctypes.POINTER(_Stencil)]
             getattr(L, f"orc_run_{t}").argtypes = [vp, vp, i, i, ctypes.POINTER(_Stencil), i]
+            getattr(L, f"orc_init_block_{t}").argtypes = [vp, i, i, i, i, i, i, i, u64]
+            getattr(L, f"orc_run_block_{t}").argtypes = [vp, vp, i, i, i, i, ctypes.POINTER(_Stencil), i, vp, vp]
         L.orc_fnv1a.restype = u64
         L.orc_fnv1a.argtypes = [vp, ctypes.c_size_t]
         _oracle = L
@@ -120,6 +122,57 @@ def run(grid: np.ndarray, kind: int, radius: int, weights, steps: int) -> np.nda
     fn(_ptr(g), _ptr(out), sz, radius, ctypes.byref(st), steps)
     del keep
     return out
+
+
+def init_block(lo, hi, seed: int, dtype=np.float32) -> np.ndarray:
+    """init_grid values of the padded-grid box [lo, hi) (2 or 3 per-dim bounds)."""
+    dim = len(lo)
+    shape = tuple(b - a for a, b in zip(lo, hi))
+    g = np.empty(shape, dtype=dtype)
+    z0, y0, x0 = (0,) + tuple(lo) if dim == 2 else tuple(lo)
+    nz, ny, nx = (1,) + shape if dim == 2 else shape
+    fn = lib().orc_init_block_f32 if dtype == np.float32 else lib().orc_init_block_f64
+    fn(_ptr(g), dim, z0, y0, x0, nz, ny, nx, seed)
+    return g
+
+
+def run_block(block: np.ndarray, kind: int, radius: int, weights, steps: int, window=None) -> np.ndarray:
+    """run() on a rectangular padded block whose outer `radius` cells are held.
+    window=(lo, hi) (block coordinates): only that window's dependency cone is
+    evolved; only the window of the result is meaningful."""
+    dim = block.ndim
+    st, keep = _stencil(kind, dim, radius, weights)
+    g = np.ascontiguousarray(block)
+    out = np.empty_like(g)
+    nz, ny, nx = (1,) + g.shape if dim == 2 else g.shape
+    fn = lib().orc_run_block_f32 if g.dtype == np.float32 else lib().orc_run_block_f64
+    wl = wh = None
+    if window is not None:
+        lo, hi = window
+        if dim == 2:
+            lo, hi = (0,) + tuple(lo), (1,) + tuple(hi)
+        wl = (ctypes.c_int * 3)(*lo)
+        wh = (ctypes.c_int * 3)(*hi)
+    fn(_ptr(g), _ptr(out), nz, ny, nx, radius, ctypes.byref(st), steps,
+       ctypes.cast(wl, ctypes.c_void_p) if wl else None, ctypes.cast(wh, ctypes.c_void_p) if wh else None)
+    del keep
+    return out
+
+
+def window_expected(init_window, sz: int, radius: int, steps: int, lo, hi, kind: int, weights, dim: int = 2):
+    """Light-cone check of a full-size run: the exact state after `steps` of the
+    padded-grid window [lo, hi) (per-dim tuples), computed from a cut-out with a
+    margin of radius*(steps+1) (clipped at the grid edge, where the real ring is
+    held). `init_window(lo, hi)` returns the initial padded-grid values of a box."""
+    p = sz + 2 * radius
+    m = radius * (steps + 1)
+    clo = tuple(max(0, a - m) for a in lo)
+    chi = tuple(min(p, b + m) for b in hi)
+    cut = init_window(clo, chi)
+    wlo = tuple(a - c for a, c in zip(lo, clo))
+    whi = tuple(b - c for b, c in zip(hi, clo))
+    out = run_block(cut, kind, radius, weights, steps, (wlo, whi))
+    return np.ascontiguousarray(out[tuple(slice(a, b) for a, b in zip(wlo, whi))])
 
 
 def step(grid: np.ndarray, kind: int, radius: int, weights) -> np.ndarray:

@@ -51,6 +51,24 @@ void orc_init_f64(double* g, int dim, int sz, int r, uint64_t seed) {
         g[i++] = (double)(dim == 3 ? orc_cell_value3(seed, z, y, x) : orc_cell_value(seed, y, x));
 }
 
+/* init_grid values of the box [z0,z0+nz) x [y0,y0+ny) x [x0,x0+nx) of the
+ * padded grid (dim 2: z ignored, nz = 1). */
+void orc_init_block_f32(float* g, int dim, int z0, int y0, int x0, int nz, int ny, int nx, uint64_t seed) {
+  size_t i = 0;
+  for (int z = z0; z < z0 + nz; ++z)
+    for (int y = y0; y < y0 + ny; ++y)
+      for (int x = x0; x < x0 + nx; ++x)
+        g[i++] = dim == 3 ? orc_cell_value3(seed, z, y, x) : orc_cell_value(seed, y, x);
+}
+
+void orc_init_block_f64(double* g, int dim, int z0, int y0, int x0, int nz, int ny, int nx, uint64_t seed) {
+  size_t i = 0;
+  for (int z = z0; z < z0 + nz; ++z)
+    for (int y = y0; y < y0 + ny; ++y)
+      for (int x = x0; x < x0 + nx; ++x)
+        g[i++] = (double)(dim == 3 ? orc_cell_value3(seed, z, y, x) : orc_cell_value(seed, y, x));
+}
+
 /* The per-point rule, written once per element type. Box: accumulator starts
  * at +0 and takes one fused multiply-add per tap in canonical order
  * (proj/src/stencil.cpp:137-143; dz outermost for 3D). Star: the same chain
@@ -122,6 +140,62 @@ void orc_init_f64(double* g, int dim, int sz, int r, uint64_t seed) {
 
 ORC_DEFINE_STEP(f32, float, fmaf)
 ORC_DEFINE_STEP(f64, double, fma)
+
+/* Same per-point rule on a rectangular padded block of nz x ny x nx cells
+ * (nz = 1 for 2D) whose outer r cells in every stencil dimension are held
+ * constant -- the light-cone checker for full-size runs: a cut-out of the
+ * grid with a margin of r*steps around a window evolves that window exactly
+ * as the whole grid does (per-point arithmetic depends only on the
+ * (2r+1)^dim neighbourhood; the contamination from the held margin travels r
+ * cells per step). */
+#define ORC_DEFINE_BLOCK(SUFFIX, T)                                                  \
+  void orc_run_block_##SUFFIX(const T* g, T* out, int nz, int ny, int nx, int r,     \
+                              const orc_stencil* st, int steps, const int* wlo,      \
+                              const int* whi) {                                      \
+    const size_t n = (size_t)nz * ny * nx;                                           \
+    const size_t sy = (size_t)nx, splane = (size_t)nx * ny;                          \
+    T* a = (T*)malloc(n * sizeof(T));                                                \
+    T* b = (T*)malloc(n * sizeof(T));                                                \
+    memcpy(a, g, n * sizeof(T));                                                     \
+    memcpy(b, g, n * sizeof(T));                                                     \
+    T* src = a;                                                                      \
+    T* dst = b;                                                                      \
+    const int d3 = st->dim == 3;                                                     \
+    const int ext[3] = {nz, ny, nx};                                                 \
+    for (int s = 1; s <= steps; ++s) {                                               \
+      /* only the cells the window still depends on: window +- r*(steps-s) */        \
+      int lo[3], hi[3];                                                              \
+      for (int k = 0; k < 3; ++k) {                                                  \
+        lo[k] = r;                                                                   \
+        hi[k] = ext[k] - r;                                                          \
+        if (wlo && whi) {                                                            \
+          const int gr = r * (steps - s);                                            \
+          if (wlo[k] - gr > lo[k]) lo[k] = wlo[k] - gr;                              \
+          if (whi[k] + gr < hi[k]) hi[k] = whi[k] + gr;                              \
+        }                                                                            \
+      }                                                                              \
+      if (!d3) {                                                                     \
+        lo[0] = 0;                                                                   \
+        hi[0] = 1;                                                                   \
+      }                                                                              \
+      _Pragma("omp parallel for collapse(2) schedule(static)")                       \
+      for (int z = lo[0]; z < hi[0]; ++z)                                            \
+        for (int y = lo[1]; y < hi[1]; ++y)                                          \
+          for (int x = lo[2]; x < hi[2]; ++x) {                                      \
+            const size_t c = (size_t)z * splane + (size_t)y * sy + (size_t)x;        \
+            dst[c] = orc_point_##SUFFIX(src, c, sy, splane, r, st->dim, st->kind, st->w); \
+          }                                                                          \
+      T* t = src;                                                                    \
+      src = dst;                                                                     \
+      dst = t;                                                                       \
+    }                                                                                \
+    memcpy(out, src, n * sizeof(T));                                                 \
+    free(a);                                                                         \
+    free(b);                                                                         \
+  }
+
+ORC_DEFINE_BLOCK(f32, float)
+ORC_DEFINE_BLOCK(f64, double)
 
 uint64_t orc_fnv1a(const void* data, size_t bytes) {
   const unsigned char* p = (const unsigned char*)data;

@@ -46,6 +46,10 @@ float orc_cell_value3(uint64_t seed, int z, int y, int x);
 void orc_init_f32(float* g, int dim, int sz, int r, uint64_t seed);
 void orc_init_f64(double* g, int dim, int sz, int r, uint64_t seed);
 
+/* init values of a box of the padded grid (dim 2: z0 ignored, nz = 1) */
+void orc_init_block_f32(float* g, int dim, int z0, int y0, int x0, int nz, int ny, int nx, uint64_t seed);
+void orc_init_block_f64(double* g, int dim, int z0, int y0, int x0, int nz, int ny, int nx, uint64_t seed);
+
 /* proj/src/stencil.cpp:146-160 (apply_step) generalised: one step over the
  * full interior, reading `in`, writing `out` (ring cells of out untouched). */
 void orc_step_f32(const float* in, float* out, int sz, int r, const orc_stencil* st);
@@ -55,6 +59,17 @@ void orc_step_f64(const double* in, double* out, int sz, int r, const orc_stenci
  * result written to `out` (may alias `g`). */
 void orc_run_f32(const float* g, float* out, int sz, int r, const orc_stencil* st, int steps);
 void orc_run_f64(const double* g, double* out, int sz, int r, const orc_stencil* st, int steps);
+
+/* run_reference on a rectangular padded block (nz = 1 for dim 2): the outer
+ * r cells of every stencil dimension are held constant. Used to check
+ * windows of full-size runs (light-cone property, see so2dr_oracle.c). */
+void orc_run_block_f32(const float* g, float* out, int nz, int ny, int nx, int r,
+                       const orc_stencil* st, int steps, const int* wlo, const int* whi);
+void orc_run_block_f64(const double* g, double* out, int nz, int ny, int nx, int r,
+                       const orc_stencil* st, int steps, const int* wlo, const int* whi);
+/* (wlo/whi: optional [z,y,x] window in block coordinates (z = 0..1 for 2D);
+ * when given, step s only updates the window grown by r*(steps-s) -- the
+ * cells the window still depends on; other cells of `out` are stale.) */
 
 /* proj/src/stencil.cpp:176-186 -- FNV-1a 64 over raw bytes. */
 uint64_t orc_fnv1a(const void* data, size_t bytes);

@@ -59,6 +59,7 @@ struct K1Args2D {
   int xorg;         // column of lane 0 cell 0 of warp 0 (aligned to VEC)
   int warps_x;      // strips along x
   int nseg;         // row segments; work items = warps_x * nseg
+  int nl, nr;       // leading / trailing strips that own ring columns (slow path)
   int cpb;          // cp.async piece bytes (16/8/4): largest dividing the pitch
   unsigned* counter;  // work-item counter (zeroed before the launch)
   T w[81];          // (2R+1)^2 weights, canonical order
@@ -651,6 +652,26 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
   cp_async_wait<0>();
 }
 
+// Work item -> (strip, segment). The strips that own ring columns run the
+// general (range-checked) path for their whole height and cost several times
+// a steady-state item, so they are handed out FIRST (longest items first):
+// fetched last they left one SM running alone for ~25% of the launch
+// (profiles/r01_baseline/k1_full.json: SM active avg 73.5% of elapsed).
+template <typename T>
+__device__ __forceinline__ void k1_item_coords(const K1Args2D<T>& a, int item, int& wx, int& sg) {
+  const int ne = a.nl + a.nr;
+  if (item < ne * a.nseg) {
+    sg = item / ne;
+    const int j = item - sg * ne;
+    wx = j < a.nl ? j : a.warps_x - ne + j;
+  } else {
+    const int inner = a.warps_x - ne;
+    const int i = item - ne * a.nseg;
+    sg = i / inner;
+    wx = a.nl + (i - sg * inner);
+  }
+}
+
 // Persistent warps with dynamic work distribution: every warp of a
 // one-wave grid fetches (strip, segment) items from an atomic counter, so the
 // SMs stay busy until the last item (no partial last wave).
@@ -664,7 +685,9 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
     if (lane == 0) item = static_cast<int>(atomicAdd(a.counter, 1u));
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= total) break;
-    k1_item<T, R, S, KIND, V, NT>(a, item % a.warps_x, item / a.warps_x, ring);
+    int wx, sg;
+    k1_item_coords(a, item, wx, sg);
+    k1_item<T, R, S, KIND, V, NT>(a, wx, sg, ring);
   }
 }
 
@@ -678,7 +701,9 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d_pk(const K1Args2D<float
     if (lane == 0) item = static_cast<int>(atomicAdd(a.counter, 1u));
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= total) break;
-    k1_item_pk<R, S, KIND, V, NT>(a, item % a.warps_x, item / a.warps_x, ring);
+    int wx, sg;
+    k1_item_coords(a, item, wx, sg);
+    k1_item_pk<R, S, KIND, V, NT>(a, wx, sg, ring);
   }
 }
 

@@ -68,6 +68,18 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   a.xorg = floor_div(L.x0 - H, VEC) * VEC;
   const int width = L.x1 - (a.xorg + H);
   a.warps_x = std::max(1, (width + a.strip - 1) / a.strip);
+  // strips whose 32V columns reach outside the interior (warp_ring in k1_item)
+  {
+    int nl = 0, nr = 0;
+    for (int wx = 0; wx < a.warps_x && a.xorg + wx * a.strip < L.ix0; ++wx) ++nl;
+    for (int wx = a.warps_x - 1; wx >= nl && a.xorg + wx * a.strip + 32 * V > L.ix1; --wx) ++nr;
+    a.nl = nl;
+    a.nr = nr;
+    if (nl + nr >= a.warps_x) {  // every strip is slow: plain order
+      a.nl = a.warps_x;
+      a.nr = 0;
+    }
+  }
   constexpr int NW = NT / 32;
   const int height = L.y1 - L.y0;
   // One wave of persistent CTAs; warps pull (strip, segment) items from a

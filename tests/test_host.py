@@ -234,3 +234,31 @@ def test_checksum_helper():
     import pyoracle
 
     assert so2dr.grid_checksum(a) == pyoracle.fnv1a(a)
+
+
+@pytest.mark.parametrize("dim,dtype,kind,r", [(2, np.float32, "box", 1), (2, np.float32, "box", 2),
+                                              (2, np.float32, "gradient", 1), (2, np.float64, "star", 2),
+                                              (3, np.float32, "star", 1), (3, np.float32, "box", 1)])
+def test_light_cone_window_checker_equals_whole_grid_oracle(oracle, dim, dtype, kind, r):
+    """The full-size GPU parity tests check windows of a huge grid against a
+    cut-out evolved by the oracle (pyoracle.window_expected). Pin that checker
+    against the whole-grid oracle: interior, edge and corner windows."""
+    o = oracle
+    sz, steps = (40, 5) if dim == 2 else (16, 3)
+    kcode = {"box": o.BOX, "star": o.STAR, "gradient": o.GRADIENT}[kind]
+    if kind == "box":
+        w = o.box_weights(r, dim)
+    elif kind == "star":
+        w = o.star_weights(r, dim)
+    else:
+        w = None
+    full = o.run(o.init_grid(sz, r, 42, dim, dtype), kcode, r, w, steps)
+    p = sz + 2 * r
+    wins = [(0, 6), (p // 2 - 3, p // 2 + 3), (p - 5, p)]
+    import itertools
+    for box in itertools.product(wins, repeat=dim):
+        lo = tuple(b[0] for b in box)
+        hi = tuple(b[1] for b in box)
+        got = o.window_expected(lambda a, b: o.init_block(a, b, 42, dtype), sz, r, steps, lo, hi, kcode, w, dim)
+        want = full[tuple(slice(a, b) for a, b in zip(lo, hi))]
+        assert np.array_equal(got.view(np.uint8), np.ascontiguousarray(want).view(np.uint8)), (lo, hi)

@@ -17,6 +17,18 @@ for s in $steps; do
     refarm)
       timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > $OUT/bench_ref.log 2>&1; echo "ref rc=$?" >> $OUT/summary.txt
       tail -1 $OUT/bench_ref.log >> $OUT/summary.txt ;;
+    k1)
+      SZ=32768 STENCILS=box2d1r,star2d1r KS=1,2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_bench.log 2>&1
+      echo "k1 rc=$?" >> $OUT/summary.txt; cat $OUT/k1_bench.log >> $OUT/summary.txt ;;
+    pipe)
+      timeout 1200 python tools/pipe_sweep.py > $OUT/pipe_sweep.log 2>&1
+      echo "pipe rc=$?" >> $OUT/summary.txt; cat $OUT/pipe_sweep.log >> $OUT/summary.txt ;;
+    ncuk1)
+      for k in 4 8; do
+        timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_stencil2d -s 1 -c 1 -o $OUT/k1_incore_k$k -f \
+          python tools/k1_one.py $k 32768 box > $OUT/k1_incore_k$k.log 2>&1
+        echo "ncuk1 k=$k rc=$?" >> $OUT/summary.txt
+      done ;;
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
         python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-value-leg > $OUT/launches_bench.log 2>&1
