@@ -162,6 +162,32 @@ __device__ __forceinline__ int row_cpb(const void* row_start) {
   return (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : 4;
 }
 
+// Steady-state copy of a lane's VB bytes (VB = V * sizeof(T), all columns
+// inside the row): the largest pieces (16/8/4 bytes) the lane's address
+// allows (dense rows of an odd-multiple-of-8-byte pitch alternate 16/8). No
+// per-element range checks.
+template <int VB>
+__device__ __forceinline__ void issue_inrow(void* dst, const void* src) {
+  char* d = static_cast<char*>(dst);
+  const char* g = static_cast<const char*>(src);
+  if constexpr (VB >= 16) {
+    if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+#pragma unroll
+      for (int b = 0; b < VB; b += 16) cp_async<16>(d + b, g + b);
+      return;
+    }
+  }
+  if constexpr (VB >= 8) {
+    if ((reinterpret_cast<uintptr_t>(g) & 7) == 0) {
+#pragma unroll
+      for (int b = 0; b < VB; b += 8) cp_async<8>(d + b, g + b);
+      return;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < VB; b += 4) cp_async<4>(d + b, g + b);
+}
+
 template <typename T, int R, int S, int KIND, int V, int NT>
 struct K1Plan2D {
   // prefetch ring depth (rows per lane; power of two; <= 32 KB of smem)
@@ -236,7 +262,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
   // ---- prefetch (each lane reads back only what it copied: no barrier) ------
   T* my_ring = &ring[0][tid * V];
   const T* src_col = a.in + xt;
-  auto issue = [&](int row) {
+  auto issue = [&](int row) SO2DR_INLINE {
     const bool ok = row < hi0;  // rows below lo0 never requested
     T* dst = my_ring + (row & (kRing - 1)) * (NT * V);
     const T* src = src_col + (int64_t)(row - sy0) * a.pitch;
@@ -246,6 +272,12 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
       if (ok) issue_vec<T, VEC>(dst + v, src + v, cpb, xt + v, a.pitch);
     cp_async_commit();
   };
+  auto issue_fast = [&](int row) SO2DR_INLINE {
+    if (row < hi0)
+      issue_inrow<V * (int)sizeof(T)>(my_ring + (row & (kRing - 1)) * (NT * V),
+                                      src_col + (int64_t)(row - sy0) * a.pitch);
+    cp_async_commit();
+  };
 #pragma unroll
   for (int d = 0; d < kRing - 1; ++d) issue(lo0 + d);
 
@@ -253,7 +285,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
   T* __restrict__ gout = a.out;
 
   // pass-through value of cell (row, xt+k) from the read buffer
-  auto passthru = [&](int row, int k) -> T {
+  auto passthru = [&](int row, int k) SO2DR_INLINE -> T {
     const int x = xt + k;
     if (x < 0 || x >= a.cols) return T(0);
     return __ldg(gin + (int64_t)(row - sy0) * a.pitch + x);
@@ -262,7 +294,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
   // One pipeline iteration at compile-time phase PH = it mod E. FAST = steady
   // state: every stage consumes and emits an interior row and the strip owns
   // no pass-through column, so all range checks compile away.
-  auto body = [&](auto phase_tag, auto fast_tag, int it) {
+  auto body = [&](auto phase_tag, auto fast_tag, int it) SO2DR_INLINE {
     constexpr int PH = decltype(phase_tag)::value;
     constexpr bool FAST = decltype(fast_tag)::value;
     const int row0 = lo0 + it;
@@ -392,7 +424,10 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
     }
 
     // stage 0: row lo0 + it arrives from the cp.async ring
-    issue(row0 + kRing - 1);
+    if constexpr (FAST)
+      issue_fast(row0 + kRing - 1);
+    else
+      issue(row0 + kRing - 1);
     cp_async_wait<kRing - 1>();
     if (FAST || row0 < hi0) {
       const T* src = my_ring + (row0 & (kRing - 1)) * (NT * V);
@@ -415,7 +450,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
   if (warp_ring) f_hi = f_lo;
 
   int it = 0;
-  auto run_general = [&](int stop) {
+  auto run_general = [&](int stop) SO2DR_INLINE {
     while (it < stop) {
       [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
         ((it < stop ? (body(std::integral_constant<int, Ps>{}, std::false_type{}, it), ++it, void())
@@ -511,7 +546,7 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
 
   T* my_ring = &ring[0][tid * V];
   const T* src_col = a.in + xt;
-  auto issue = [&](int row) {
+  auto issue = [&](int row) SO2DR_INLINE {
     const bool ok = row < hi0;
     T* dst = my_ring + (row & (kRing - 1)) * (NT * V);
     const T* src = src_col + (int64_t)(row - sy0) * a.pitch;
@@ -521,16 +556,23 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
       if (ok) issue_vec<T, VEC>(dst + v, src + v, cpb, xt + v, a.pitch);
     cp_async_commit();
   };
+  // steady state: the strip owns no column outside the interior
+  auto issue_fast = [&](int row) SO2DR_INLINE {
+    if (row < hi0)
+      issue_inrow<V * (int)sizeof(T)>(my_ring + (row & (kRing - 1)) * (NT * V),
+                                      src_col + (int64_t)(row - sy0) * a.pitch);
+    cp_async_commit();
+  };
 #pragma unroll
   for (int d = 0; d < kRing - 1; ++d) issue(lo0 + d);
 
-  auto passthru = [&](int row, int k) -> T {
+  auto passthru = [&](int row, int k) SO2DR_INLINE -> T {
     const int x = xt + k;
     if (x < 0 || x >= a.cols) return T(0);
     return __ldg(a.in + (int64_t)(row - sy0) * a.pitch + x);
   };
 
-  auto body = [&](auto phase_tag, auto fast_tag, int it) {
+  auto body = [&](auto phase_tag, auto fast_tag, int it) SO2DR_INLINE {
     constexpr int PH = decltype(phase_tag)::value;
     constexpr bool FAST = decltype(fast_tag)::value;
     const int row0 = lo0 + it;
@@ -609,7 +651,10 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
         }
       }
     }
-    issue(row0 + kRing - 1);
+    if constexpr (FAST)
+      issue_fast(row0 + kRing - 1);
+    else
+      issue(row0 + kRing - 1);
     cp_async_wait<kRing - 1>();
     if (FAST || row0 < hi0) {
       const T* src = my_ring + (row0 & (kRing - 1)) * (NT * V);
@@ -630,7 +675,7 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
   if (warp_ring) f_hi = f_lo;
 
   int it = 0;
-  auto run_general = [&](int stop) {
+  auto run_general = [&](int stop) SO2DR_INLINE {
     while (it < stop) {
       [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
         ((it < stop ? (body(std::integral_constant<int, Ps>{}, std::false_type{}, it), ++it, void())

@@ -9,6 +9,7 @@
 #include <utility>
 
 #include "k1_2d.cuh"
+#include "k1_2d_p2.cuh"
 #include "k1_launch.h"
 
 namespace so2dr_dev {
@@ -35,6 +36,17 @@ inline int k1_v_override() {
   static int v = [] {
     const char* s = std::getenv("SO2DR_K1_V");
     return s ? std::atoi(s) : 0;
+  }();
+  return v;
+}
+
+// Experiment knob: SO2DR_K1_IMPL=p2 selects the paired-strip packed kernel
+// (k1_2d_p2.cuh) for fp32 box/star, =pk the single-strip packed kernel.
+inline int k1_impl_override() {
+  static int v = [] {
+    const char* s = std::getenv("SO2DR_K1_IMPL");
+    if (!s) return 0;
+    return std::strcmp(s, "p2") == 0 ? 2 : std::strcmp(s, "pk") == 0 ? 1 : 0;
   }();
   return v;
 }
@@ -113,6 +125,69 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// Paired-strip launch (k1_2d_p2.cuh): one warp item = two strips x one row
+// segment; same geometry rules as launch_2d_fixed.
+template <int R, int S, int KIND, int V, int MINB>
+cudaError_t launch_2d_p2(const K1Launch& L, cudaStream_t stream) {
+  constexpr int NT = kThreads2D;
+  constexpr int H = R * S;
+  constexpr int VEC = (V * 4) >= 16 ? 4 : V;
+  using P = K1PlanP2<R, S, KIND, V, NT>;
+  K1Args2D<float> a;
+  a.in = static_cast<const float*>(L.in);
+  a.out = static_cast<float*>(L.out);
+  a.pitch = L.pitch;
+  a.base = L.base;
+  a.rows = L.rows;
+  a.cols = L.cols;
+  a.y0 = L.y0, a.y1 = L.y1, a.x0 = L.x0, a.x1 = L.x1;
+  a.iy0 = L.iy0, a.iy1 = L.iy1, a.ix0 = L.ix0, a.ix1 = L.ix1;
+  constexpr int E = 2 * R + 1;
+  for (int i = 0; i < 81; ++i) a.w[i] = 0.f;
+  if (L.w)
+    for (int i = 0; i < E * E; ++i) a.w[i] = static_cast<float>(L.w[i]);
+  {
+    const int64_t pb = L.pitch * 4;
+    a.cpb = pb % 16 == 0 ? 16 : pb % 8 == 0 ? 8 : 4;
+  }
+  a.strip = ((32 * V - 2 * H) / VEC) * VEC;
+  if (a.strip <= 0) return cudaErrorInvalidValue;
+  a.xorg = floor_div(L.x0 - H, VEC) * VEC;
+  const int width = L.x1 - (a.xorg + H);
+  a.warps_x = std::max(1, (width + a.strip - 1) / a.strip);
+  {
+    int nl = 0, nr = 0;
+    for (int wx = 0; wx < a.warps_x && a.xorg + wx * a.strip < L.ix0; ++wx) ++nl;
+    for (int wx = a.warps_x - 1; wx >= nl && a.xorg + wx * a.strip + 32 * V > L.ix1; --wx) ++nr;
+    a.nl = nl;
+    a.nr = nr;
+  }
+  constexpr int NW = NT / 32;
+  const int height = L.y1 - L.y0;
+  auto kern = k1_stencil2d_p2<R, S, KIND, V, NT, MINB>;
+  static int occ = 0;
+  if (occ == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+    if (e != cudaSuccess) return e;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, P::SMEM) != cudaSuccess || occ < 1) occ = 1;
+  }
+  const int sms = device_sm_count();
+  const int np = (a.warps_x + 1) / 2;
+  const int resident_warps = sms * occ * NW;
+  const int min_seg = std::max(48, 6 * (H + S * (R + 1)));
+  const int max_ns = std::max(1, height / min_seg);
+  int ns = std::max(1, (8 * resident_warps + np - 1) / np);
+  ns = std::min(ns, max_ns);
+  a.seg = (height + ns - 1) / ns;
+  a.nseg = (height + a.seg - 1) / a.seg;
+  a.counter = k1_next_counter(stream);
+  if (!a.counter) return cudaErrorUnknown;
+  const int items = np * a.nseg;
+  const int ctas = std::max(1, std::min(sms * occ, (items + NW - 1) / NW));
+  kern<<<ctas, NT, P::SMEM, stream>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, int R, int KIND, int S = 1>
 cudaError_t launch_2d_s(const K1Launch& L, cudaStream_t stream) {
   if constexpr (S > maxs2d<T>(R)) {
@@ -121,6 +196,12 @@ cudaError_t launch_2d_s(const K1Launch& L, cudaStream_t stream) {
     if (L.steps == S) {
       if constexpr (sizeof(T) == 4 && R == 1 && KIND != KGRAD) {
         if (k1_v_override() == 2) return launch_2d_fixed<T, R, S, KIND, 2, 2>(L, stream);
+        if (k1_impl_override() == 2) {
+          if constexpr (S <= 4)
+            return launch_2d_p2<R, S, KIND, 4, 1>(L, stream);
+          else
+            return launch_2d_p2<R, S, KIND, 2, 1>(L, stream);
+        }
       }
       return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1>(L, stream);
     }

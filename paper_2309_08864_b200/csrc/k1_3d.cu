@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
 #pragma unroll
       for (int k = 0; k < V; ++k) cur[u][j][k] = T(0);
 
-  auto issue = [&](int plane) {
+  auto issue = [&](int plane) SO2DR_INLINE {
     const bool ok = plane < hi0;
     const T* src = a.in + (int64_t)(plane - sz0) * a.plane_stride;
 #pragma unroll
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
   for (int d = 0; d < RING - 1; ++d) issue(lo0 + d);
   __syncthreads();
 
-  auto passthru = [&](int plane, int j, int k) -> T {
+  auto passthru = [&](int plane, int j, int k) SO2DR_INLINE -> T {
     const int x = xt + k, y = yt + j;
     if (x < 0 || x >= a.p || y < 0 || y >= a.p) return T(0);
     return __ldg(a.in + (int64_t)(plane - sz0) * a.plane_stride + (int64_t)y * a.pitch + x);
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
       }
   };
 
-  auto body = [&](auto phase_tag, int it) {
+  auto body = [&](auto phase_tag, int it) SO2DR_INLINE {
     constexpr int PH = decltype(phase_tag)::value;
     const int par = it & 1, ppar = par ^ 1;
     const int row0 = lo0 + it;
@@ -272,7 +272,9 @@ inline int fdiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 template <typename T, int R, int S, int KIND>
 cudaError_t launch3(const K1Launch& L, cudaStream_t stream) {
-  constexpr int NT = 512, NW = NT / 32, V = 2, VY = 2, H = R * S;
+  // 512 threads cap registers at 128; the fp64 radius-2 box needs more (a spill
+  // otherwise), so it runs 256-thread CTAs
+  constexpr int NT = (sizeof(T) == 8 && R == 2) ? 256 : 512, NW = NT / 32, V = 2, VY = 2, H = R * S;
   constexpr size_t smem = sizeof(T) * (4 * VY * NT * V + 2 * S * (NW + 2) * 2 * R * 32 * V);
   static_assert(smem <= 227 * 1024, "3D K1 shared memory");
   auto kern = k1_stencil3d<T, R, S, KIND, V, VY, NT>;

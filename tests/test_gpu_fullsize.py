@@ -105,8 +105,8 @@ def test_config3_star3d1r_fullsize_out_of_core(eng16, oracle):
 
 
 def test_config4_box3d1r_fullsize_slab(eng16, oracle):
-    """BASELINE configs[3] per-GPU slab shape: box3d1r fp32, sz=2048, d=16, S_TB=16, k_on=4, n=32."""
-    _check_fullsize(eng16, oracle, 3, np.float32, "box", 1, 2048, 16, 16, 4, 32, 6, 2, 8)
+    """BASELINE configs[3] per-GPU slab shape: box3d1r fp32, sz=2048, d=32 (d=16 needs 17.8 GB of ping-pong buffers), S_TB=16, k_on=4, n=32."""
+    _check_fullsize(eng16, oracle, 3, np.float32, "box", 1, 2048, 32, 16, 4, 32, 6, 2, 8)
 
 
 def test_config5_star2d2r_f64_fullsize(eng16, oracle):

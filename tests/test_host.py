@@ -262,3 +262,20 @@ def test_light_cone_window_checker_equals_whole_grid_oracle(oracle, dim, dtype, 
         got = o.window_expected(lambda a, b: o.init_block(a, b, 42, dtype), sz, r, steps, lo, hi, kcode, w, dim)
         want = full[tuple(slice(a, b) for a, b in zip(lo, hi))]
         assert np.array_equal(got.view(np.uint8), np.ascontiguousarray(want).view(np.uint8)), (lo, hi)
+
+
+def test_no_kernel_uses_local_memory():
+    """Every sm_100a kernel in the library keeps its pipeline state in registers:
+    a stack frame means a spilled or out-of-line (CALL) pipeline, which ran the
+    fp64 star kernels 25x slower before SO2DR_INLINE (k1_launch.h)."""
+    import shutil
+    import subprocess
+
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([cuobjdump, "-res-usage", so2dr.LIB_PATH], capture_output=True, text=True).stdout
+    funcs = re.findall(r"Function (\S+):\s*\n\s*REG:(\d+) STACK:(\d+)", out)
+    assert len(funcs) > 50
+    bad = [(f, s) for f, _, s in funcs if int(s) != 0]
+    assert not bad, bad[:5]

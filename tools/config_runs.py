@@ -3,7 +3,7 @@ end to end through the C ABI (pinned host grid, all H2D/D2H inside the timing).
 
   cfg1  star2d1r fp32 4096^2, d=4, n=8, S_TB=4, k_on=4 (the CPU-reference preset)
   cfg3  star3d1r fp32 sz=2048 (34.5 GB, ~2x a 16 GiB budget), d=16, S_TB=8, n=64, k_on 1/2/4/8
-  cfg4  box3d1r fp32 per-GPU slab of the 8-GPU config: sz=2048, d=16, S_TB=16, k_on=4, n=32
+  cfg4  box3d1r fp32 per-GPU slab of the 8-GPU config: sz=2048, d=32, S_TB=16, k_on=4, n=32
   cfg5  star2d2r (j2d9pt-shaped) fp64 sz=65536 (34.4 GB), d=16, S_TB=64, k_on=4, n=64
 Prints one JSON line per run: GCell/s, device ms, R_pcie bound, fraction."""
 import json
@@ -60,5 +60,5 @@ if "cfg5" in which:
     run("cfg5 star2d2r fp64", 2, np.float64, so2dr.StencilSpec.star(2, w=1.0 / 9.0, dtype=np.float64), 65536, 16,
         64, [4], 64, reps=2)
 if "cfg4" in which:
-    run("cfg4 box3d1r (per-GPU slab)", 3, np.float32, so2dr.StencilSpec.box(1, dim=3), 2048, 16, 16, [4], 32,
+    run("cfg4 box3d1r (per-GPU slab)", 3, np.float32, so2dr.StencilSpec.box(1, dim=3), 2048, 32, 16, [4], 32,
         reps=1)

@@ -29,6 +29,23 @@ for s in $steps; do
           python tools/k1_one.py $k 32768 box > $OUT/k1_incore_k$k.log 2>&1
         echo "ncuk1 k=$k rc=$?" >> $OUT/summary.txt
       done ;;
+    full)
+      timeout 1500 python -m pytest tests/test_gpu_fullsize.py -x -q -m gpu --durations=0 > $OUT/pytest_fullsize.log 2>&1
+      echo "fullsize rc=$?" >> $OUT/summary.txt; tail -12 $OUT/pytest_fullsize.log >> $OUT/summary.txt ;;
+    prof)
+      for d in 16 64; do timeout 600 python tools/pipe_profile.py 92160 $d 8 3 > $OUT/pipe_profile_d$d.log 2>&1; done
+      echo "prof rc=$?" >> $OUT/summary.txt; head -1 $OUT/pipe_profile_d16.log $OUT/pipe_profile_d64.log >> $OUT/summary.txt ;;
+    configs)
+      timeout 1500 python tools/config_runs.py $CONFIGS > $OUT/config_runs.log 2>&1
+      echo "configs rc=$?" >> $OUT/summary.txt; cat $OUT/config_runs.log >> $OUT/summary.txt ;;
+    pcie)
+      timeout 300 python tools/pcie_probe.py > $OUT/pcie_probe.log 2>&1; echo "pcie rc=$?" >> $OUT/summary.txt
+      cat $OUT/pcie_probe.log >> $OUT/summary.txt ;;
+    p2)
+      SO2DR_K1_IMPL=p2 timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py -x -q > $OUT/pytest_p2.log 2>&1
+      echo "pytest p2 rc=$?" >> $OUT/summary.txt; tail -2 $OUT/pytest_p2.log >> $OUT/summary.txt
+      SO2DR_K1_IMPL=p2 SZ=32768 STENCILS=box2d1r,star2d1r KS=1,2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_bench_p2.log 2>&1
+      echo "k1 p2 rc=$?" >> $OUT/summary.txt; cat $OUT/k1_bench_p2.log >> $OUT/summary.txt ;;
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
         python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-value-leg > $OUT/launches_bench.log 2>&1
