@@ -4,7 +4,7 @@
 
 Workload (BASELINE configs[1]): box2d1r fp32 out-of-core, grid ~2x the device
 budget on one B200, 64 timesteps: sz=92160 (92162^2 fp32 = 33.98 GB host grid),
-16 GiB real HBM budget, d=16 chunks, S_TB=64 (one round), k_on=8, N_strm=3.
+16 GiB real HBM budget, d=64 chunks, S_TB=64 (one round), k_on=4, N_strm=3.
 A "step" is one full so2dr run (64 timesteps over the whole grid).
 
   value : same run with the grid already resident in HBM (copies become D2D)
@@ -37,7 +37,14 @@ import numpy as np  # noqa: E402
 
 METRIC = "GCell-updates/s end-to-end (incl. H2D/D2H) at 1/2/4/8 B200; % of roofline"
 UNIT = "GCell/s"
-SZ1, D_PER_RANK, S_TB, K_ON, NSTEPS, NSTRM, R = 92160, 16, 64, 8, 64, 3, 1
+# d=64 chunks (not SURVEY's worked-example 16): 4x shorter pipeline fill/drain
+# (first H2D + first chunk's kernels, last D2H) -- 780 vs 832 ms per run on
+# this box (profiles/r01_pcie); k_on=4: K1 then binds on HBM (2b/k_on = 2 B per
+# update => 3.3 TCell/s HBM roof < 3.5 TCell/s FMA roof), and e2e is unchanged
+# vs k_on=8 (the kernel is hidden behind PCIe either way).
+SZ1, D_PER_RANK, S_TB, K_ON, NSTEPS, NSTRM, R = 92160, 64, 64, 4, 64, 3, 1
+FMA_PEAK = 36.88e12  # measured FFMA2 peak on this pool's B200 (profiles/r01_pcie/fma_peak.jsonl)
+TAPS = 9  # box2d1r
 BUDGET = 16 << 30
 
 
@@ -109,8 +116,11 @@ class ClockSampler:
 
 
 def pcie_probe(torch, dev):
-    """Pinned H2D / D2H GB/s, each alone and both at once (per direction)."""
-    n = 1 << 30
+    """Pinned-host PCIe GB/s on this box, timed with CUDA events on the copy
+    streams: H2D alone, D2H alone, and both at once (2 GiB each way). In duplex
+    the host side caps the COMBINED rate (~94 GB/s here, tools/pcie_probe.py),
+    so duplex_GBps_per_dir = combined / 2 is what a balanced pipeline can use."""
+    n = 2 << 30
     h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -119,18 +129,27 @@ def pcie_probe(torch, dev):
     out = {}
     for name in ("h2d", "d2h", "duplex"):
         best = 0.0
-        for _ in range(3):
+        for _ in range(2):
             torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            s1.wait_event(e0)
+            s2.wait_event(e0)
             if name in ("h2d", "duplex"):
                 with torch.cuda.stream(s1):
                     d.copy_(h, non_blocking=True)
             if name in ("d2h", "duplex"):
                 with torch.cuda.stream(s2):
                     h2.copy_(d2, non_blocking=True)
+            torch.cuda.current_stream().wait_stream(s1)
+            torch.cuda.current_stream().wait_stream(s2)
+            e1.record()
             torch.cuda.synchronize(dev)
-            best = max(best, n / (time.perf_counter() - t0) / 1e9)
-        out[name + "_GBps_per_dir"] = best
+            moved = n * (2 if name == "duplex" else 1)
+            best = max(best, moved / e0.elapsed_time(e1) / 1e6)
+        out[name + ("_combined_GBps" if name == "duplex" else "_GBps")] = round(best, 2)
+    out["duplex_GBps_per_dir"] = round(out["duplex_combined_GBps"] / 2, 2)
     del h, h2, d, d2
     return out
 
@@ -138,12 +157,12 @@ def pcie_probe(torch, dev):
 def cpu_baseline_sample():
     """The reference's own CPU solver (oracle/_ref = /root/reference sources, -O3
     -ffp-contract=off -fopenmp) on a bounded sample of the workload: same stencil,
-    d, S_TB, k_on, n; sz reduced 8x (1/64 of the cells)."""
+    d, S_TB, k_on, n; sz reduced 3x (1/9 of the cells, ~10 s on 16 host threads)."""
     import ctypes
 
     import pyoracle as o
 
-    sz, d = SZ1 // 8, D_PER_RANK
+    sz, d = SZ1 // 3, D_PER_RANK
     cells = (sz + 2 * R) ** 2
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     if o.have_ref():
@@ -196,7 +215,7 @@ def run_reference_arm(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (splitmix64 init_grid, seed 42)",
             "config": {"workload": workload_desc(1, sz, d) + "; reference CPU solver timed on a bounded sample "
-                       "(sz/8, same d/S_TB/k_on/n)"},
+                       "(sz/3, same d/S_TB/k_on/n)"},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -322,19 +341,25 @@ def main():
 
     pk = peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
+    peak_src = ("MEASURED_PEAKS.json hbm_gbs (of measured copy)" if "hbm_gbs" in pk else
+                "of fallback: 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)")
     e2e_v = total_updates * args.steps / (e2e_res["device_ms_total"] / 1e3) / 1e9
     val_v = (total_updates * args.steps / (value_res["device_ms_total"] / 1e3) / 1e9) if value_res else None
     # K1 roofline: algorithmic bytes (input rows read once + output rows written once per launch)
     kr = e2e_res
     k_gbs = kr["alg_bytes"] / (kr["kernel_ms"] / 1e3) / 1e9 if kr["kernel_ms"] > 0 else 0.0
     per_launch = kr["alg_bytes"] / max(kr["launches"], 1)
-    traffic = None
+    traffic, traffic_src = None, None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))
-        if prof.get("k_on") == k_on:
-            traffic = prof.get("dram_bytes_per_launch")
+        if prof.get("k_on") == k_on and prof.get("d") == d:
+            # ncu DRAM bytes per launch over a steady-state window, scaled to this run's
+            # average launch by the window's measured traffic/algorithmic ratio
+            traffic = per_launch * prof["dram_over_alg"]
+            traffic_src = prof.get("source")
     except Exception:
         pass
+    k_fma = total_updates * args.steps * TAPS / (kr["kernel_ms"] / 1e3) if kr["kernel_ms"] > 0 else 0.0
     bw_dir = pc.get("duplex_GBps_per_dir", 50.0)
     r_pcie = world * bw_dir * 1e9 * S_TB / 4 / 1e9
     r_hbm = world * hbm * 1e9 / (2 * 4 / k_on + 2 * 4 / S_TB) / 1e9
@@ -367,7 +392,12 @@ def main():
                      "alg_bytes_per_launch": per_launch,
                      "avg_launch_ms": kr["kernel_ms"] / max(kr["launches"], 1),
                      "kernel_share_of_step": kr["kernel_ms"] / max(e2e_res["device_ms_total"], 1e-9),
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+                     "peak_source": peak_src, "traffic_source": traffic_src,
+                     "timing": "CUDA events bracketing every K1 launch on its own (compute) stream",
+                     "fma": {"achieved_TFMAps": k_fma / 1e12, "peak_TFMAps": FMA_PEAK / 1e12,
+                             "frac": k_fma / FMA_PEAK,
+                             "note": "useful (non-redundant) FMAs: sz^2 * n * 9 per step; peak = measured FFMA2 "
+                                     "rate (profiles/r01_pcie/fma_peak.jsonl)"}},
         "binding_roofline": {"R_pcie": r_pcie, "R_hbm": r_hbm, "R_bind": r_bind, "unit": UNIT,
                              "frac_e2e": e2e_v / r_bind, "frac_value_vs_R_hbm": (val_v / r_hbm) if val_v else None,
                              "pcie_measured": pc,

@@ -2,6 +2,7 @@
 // structs into engine requests and the library's exception types
 // (include/so2dr/errors.hpp, mirroring proj/include/so2dr/errors.hpp) into
 // so2dr_status codes plus a per-context message.
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -161,7 +162,9 @@ so2dr_status so2dr_host_alloc(so2dr_ctx* ctx, size_t bytes, void** out) {
     need_ctx(ctx);
     if (!out || !bytes) throw so2dr::ContractError("host_alloc: bad arguments");
     SO2DR_CK(cudaSetDevice(ctx->device));
-    const cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocPortable);
+    // SO2DR_HOST_ALLOC_DEFAULT=1: plain cudaHostAllocDefault (diagnostics)
+    static const bool dflt = std::getenv("SO2DR_HOST_ALLOC_DEFAULT") != nullptr;
+    const cudaError_t e = cudaHostAlloc(out, bytes, dflt ? cudaHostAllocDefault : cudaHostAllocPortable);
     if (e == cudaErrorMemoryAllocation) {
       cudaGetLastError();
       throw so2dr::OutOfDeviceMemoryError("host:pinned", bytes, 0, 0);

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -402,18 +403,32 @@ uint64_t device_footprint(const so2dr::RunConfig& cfg, const Geo& g, int n_strm)
 
 // Copy `n` units between a device field (pitch g.pitch) and the grid (host or
 // device, dense rows of g.p cells). Uses the 2D copy engine path.
+constexpr uintptr_t kPcieAlign = 128;  // bytes; see copy_units
+
 static void copy_units(const Geo& g, void* dst, int64_t dst_pitch, const void* src,
-                       int64_t src_pitch, int64_t n, cudaStream_t s) {
+                       int64_t src_pitch, int64_t n, cudaStream_t s,
+                       cudaMemcpyKind kind = cudaMemcpyDefault) {
   if (n <= 0) return;
   if (dst_pitch == g.p && src_pitch == g.p) {  // dense on both sides: one contiguous copy
-    SO2DR_CK(cudaMemcpyAsync(dst, src, static_cast<size_t>(n * g.unit_rows * g.p * g.elem),
-                             cudaMemcpyDefault, s));
+    const size_t bytes = static_cast<size_t>(n * g.unit_rows * g.p * g.elem);
+    // PCIe copies start at a 128-byte aligned HOST address: a copy whose host
+    // side starts off a 128-byte boundary runs D2H at ~42 instead of ~50 GB/s
+    // in duplex (profiles/r01_pcie). Dense rows of the grid start at any
+    // 8-byte offset, so the unaligned head (< 128 B) goes as its own copy.
+    const void* host = kind == cudaMemcpyHostToDevice ? src : kind == cudaMemcpyDeviceToHost ? dst : nullptr;
+    size_t head = host ? (kPcieAlign - (reinterpret_cast<uintptr_t>(host) & (kPcieAlign - 1))) & (kPcieAlign - 1) : 0;
+    if (head >= bytes) head = 0;
+    if (head) SO2DR_CK(cudaMemcpyAsync(dst, src, head, kind, s));
+    SO2DR_CK(cudaMemcpyAsync(static_cast<char*>(dst) + head, static_cast<const char*>(src) + head, bytes - head,
+                             kind, s));
     return;
   }
   SO2DR_CK(cudaMemcpy2DAsync(dst, dst_pitch * g.elem, src, src_pitch * g.elem,
                              static_cast<size_t>(g.p) * g.elem,
-                             static_cast<size_t>(n * g.unit_rows), cudaMemcpyDefault, s));
+                             static_cast<size_t>(n * g.unit_rows), kind, s));
 }
+
+constexpr uintptr_t kCopyAlign = 256;  // bytes; see RunCtx::congruent
 
 struct Field {
   char* buf[2] = {nullptr, nullptr};
@@ -427,6 +442,16 @@ struct RunCtx {
   int64_t host_lo;
   RunResponse& out;
   bool profile;
+  // where the grid lives: 0 host, 1 device (value leg: "transfers" are D2D),
+  // 2 managed (let the driver decide)
+  int grid_mem = 0;
+
+  cudaMemcpyKind kind_in() const {
+    return grid_mem == 0 ? cudaMemcpyHostToDevice : grid_mem == 1 ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault;
+  }
+  cudaMemcpyKind kind_out() const {
+    return grid_mem == 0 ? cudaMemcpyDeviceToHost : grid_mem == 1 ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault;
+  }
 
   char* dev_at(const Field& f, int which, int unit) const {
     return f.buf[which] + static_cast<int64_t>(unit - f.base) * g.dev_unit_elems() * g.elem;
@@ -435,17 +460,33 @@ struct RunCtx {
     return host + (static_cast<int64_t>(unit) - host_lo) * g.host_unit_elems() * g.elem;
   }
   void h2d(const Field& f, int which, RowInterval rows, cudaStream_t s) const {
-    copy_units(g, dev_at(f, which, rows.lo), g.pitch, host_at(rows.lo), g.p, rows.height(), s);
+    copy_units(g, dev_at(f, which, rows.lo), g.pitch, host_at(rows.lo), g.p, rows.height(), s, kind_in());
   }
   void d2h(const Field& f, int which, RowInterval rows, cudaStream_t s) const {
-    copy_units(g, host_at(rows.lo), g.p, dev_at(f, which, rows.lo), g.pitch, rows.height(), s);
+    copy_units(g, host_at(rows.lo), g.p, dev_at(f, which, rows.lo), g.pitch, rows.height(), s, kind_out());
   }
   void d2d(char* dst, const char* src, int64_t units, cudaStream_t s) const {
-    if (units <= 0) return;
+    // SO2DR_DIAG_NO_D2D=1: skip on-device copies (transfer diagnostics; results are wrong)
+    static const bool no_d2d = std::getenv("SO2DR_DIAG_NO_D2D") != nullptr;
+    if (units <= 0 || no_d2d) return;
     SO2DR_CK(cudaMemcpyAsync(dst, src, static_cast<size_t>(units * g.dev_unit_elems() * g.elem),
                              cudaMemcpyDeviceToDevice, s));
   }
   uint64_t bytes(int64_t units) const { return static_cast<uint64_t>(units) * g.unit_bytes(); }
+
+  // Place the chunk's device rows at the same address alignment (mod
+  // kCopyAlign) as the same rows of the grid, so every H2D / D2H is a copy
+  // between congruent addresses: the copy engine then moves whole aligned
+  // TLPs instead of re-aligning every one. (Dense host rows of odd multiples of
+  // 8 bytes start at every 8-byte offset mod 64.)
+  void congruent(Field& f, char* const raw[2]) const {
+    const uintptr_t h = reinterpret_cast<uintptr_t>(host_at(f.base));
+    for (int b = 0; b < 2; ++b) {
+      const uintptr_t r = reinterpret_cast<uintptr_t>(raw[b]);
+      const uintptr_t shift = (h - r) & (kCopyAlign - 1);
+      f.buf[b] = raw[b] + shift;
+    }
+  }
 
   // timed region helpers
   cudaEvent_t stage_begin(cudaStream_t s) const {
@@ -610,10 +651,11 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
   for (int i = cb; i < ce; ++i) max_work = std::max(max_work, lay.chunks[i].working.height());
   const uint64_t unit = static_cast<uint64_t>(g.dev_unit_elems()) * g.elem;
   std::vector<Field> F(ns);
+  std::vector<std::array<char*, 2>> raw(ns);
   for (int k = 0; k < ns; ++k)
     for (int b = 0; b < 2; ++b)
-      F[k].buf[b] = static_cast<char*>(ctx->pool.get(
-          "stream" + std::to_string(k) + ".buf" + std::to_string(b), max_work * unit));
+      raw[k][b] = static_cast<char*>(ctx->pool.get("stream" + std::to_string(k) + ".buf" + std::to_string(b),
+                                                   max_work * unit + kCopyAlign));
   std::vector<char*> slot(slots, nullptr);
   if (dl > 1)
     for (int j = 0; j < slots; ++j)
@@ -625,6 +667,11 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
   if (has_lo) band_lo = static_cast<char*>(ctx->pool.get("band.lo", h * unit));
   if (has_hi) band_hi = static_cast<char*>(ctx->pool.get("band.hi", h * unit));
   cudaStream_t s_h2d = ctx->stream(0), s_cmp = ctx->stream(1), s_d2h = ctx->stream(2);
+  static const int h2d_split = [] {  // SO2DR_H2D_SPLIT=k: experiment knob
+    const char* e = std::getenv("SO2DR_H2D_SPLIT");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  for (int k = 1; k < h2d_split; ++k) ctx->stream(4 + k);
   cudaStream_t aux_lo = ctx->stream(3), aux_hi = ctx->stream(4);
 
   std::vector<cudaEvent_t> ev_h2d(d, nullptr), ev_cmp(d, nullptr), ev_d2h(d, nullptr);
@@ -647,7 +694,7 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
       const RowInterval band{lay.fence[cb], lay.fence[cb] + h};
       wait(aux_lo, ev_d2h[cb]);
       wait(aux_lo, ev_lo_used);
-      copy_units(g, band_lo, g.pitch, rc.host_at(band.lo), g.p, h, aux_lo);
+      copy_units(g, band_lo, g.pitch, rc.host_at(band.lo), g.p, h, aux_lo, rc.kind_in());
       acc.L.htod += rc.bytes(h);
       ev_band_lo = record_sync(ctx, aux_lo);
       check_cu(cuStreamWaitValue32(aux_lo, dptr(&sl.flags[2]), epoch, CU_STREAM_WAIT_VALUE_GEQ),
@@ -660,7 +707,7 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
       const RowInterval band{lay.fence[ce] - h, lay.fence[ce]};
       wait(aux_hi, ev_d2h[ce - 1]);
       wait(aux_hi, ev_hi_used);
-      copy_units(g, band_hi, g.pitch, rc.host_at(band.lo), g.p, h, aux_hi);
+      copy_units(g, band_hi, g.pitch, rc.host_at(band.lo), g.p, h, aux_hi, rc.kind_in());
       acc.L.htod += rc.bytes(h);
       ev_band_hi = record_sync(ctx, aux_hi);
       check_cu(cuStreamWaitValue32(aux_hi, dptr(&sl.flags[3]), epoch, CU_STREAM_WAIT_VALUE_GEQ),
@@ -675,6 +722,7 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
       const int pk = (i - cb) % ns;
       Field& f = F[pk];
       f.base = ci.working.lo;
+      rc.congruent(f, raw[pk].data());
 
       // ---- H2D stream: transfer rows into buf0 of pair pk --------------------
       wait(s_h2d, ev_pair_free[pk]);  // drained by the D2H of chunk i - N_strm
@@ -689,7 +737,20 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
       if (i == cb && has_lo) tr.lo = std::max(tr.lo, lay.fence[cb] + h);
       if (i == ce - 1 && has_hi) tr.hi = lay.fence[ce] - h;
       cudaEvent_t sb = rc.stage_begin(s_h2d);
-      rc.h2d(f, 0, tr, s_h2d);
+      if (h2d_split > 1 && tr.height() >= 2 * h2d_split) {
+        // experiment: the transfer as h2d_split pieces on as many copy streams
+        cudaEvent_t go = record_sync(ctx, s_h2d);
+        const int step = (tr.height() + h2d_split - 1) / h2d_split;
+        for (int k = 0; k < h2d_split; ++k) {
+          cudaStream_t sk = k == 0 ? s_h2d : ctx->stream(4 + k);
+          if (k) wait(sk, go);
+          const RowInterval piece{tr.lo + k * step, std::min(tr.hi, tr.lo + (k + 1) * step)};
+          rc.h2d(f, 0, piece, sk);
+          if (k) wait(s_h2d, record_sync(ctx, sk));
+        }
+      } else {
+        rc.h2d(f, 0, tr, s_h2d);
+      }
       acc.L.htod += rc.bytes(tr.height());
       rc.stage_end(sb, s_h2d, t, i, Stage::htod, rc.bytes(tr.height()), 0, rec.stage,
                    rec.stage_idx);
@@ -963,6 +1024,7 @@ void run(so2dr_ctx* ctx, RunRequest& q, RunResponse& out) {
 
   // host grid: pin it for the duration of the call if it is large pageable memory
   HostPin pin;
+  int grid_mem = 0;
   {
     cudaPointerAttributes attr{};
     const cudaError_t e = cudaPointerGetAttributes(&attr, q.grid);
@@ -975,6 +1037,7 @@ void run(so2dr_ctx* ctx, RunRequest& q, RunResponse& out) {
       units = hi - lo;
     }
     const size_t bytes = static_cast<size_t>(units) * g.host_unit_elems() * g.elem;
+    if (e == cudaSuccess) grid_mem = attr.type == cudaMemoryTypeDevice ? 1 : attr.type == cudaMemoryTypeManaged ? 2 : 0;
     if (e == cudaSuccess && attr.type == cudaMemoryTypeUnregistered && bytes >= (32u << 20) &&
         cfg.n > 0) {
       if (cudaHostRegister(q.grid, bytes, cudaHostRegisterDefault) == cudaSuccess) {
@@ -988,6 +1051,7 @@ void run(so2dr_ctx* ctx, RunRequest& q, RunResponse& out) {
 
   const int ns = cfg.n_strm;
   RunCtx rc{ctx, g, static_cast<char*>(q.grid), q.host_lo, out, ctx->profiling};
+  rc.grid_mem = grid_mem;
   Acc acc;
   Recorder rec;
   cudaStream_t s0 = ctx->stream(0);

@@ -127,9 +127,8 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
 
 // Paired-strip launch (k1_2d_p2.cuh): one warp item = two strips x one row
 // segment; same geometry rules as launch_2d_fixed.
-template <int R, int S, int KIND, int V, int MINB>
+template <int R, int S, int KIND, int V, int NT, int MINB>
 cudaError_t launch_2d_p2(const K1Launch& L, cudaStream_t stream) {
-  constexpr int NT = kThreads2D;
   constexpr int H = R * S;
   constexpr int VEC = (V * 4) >= 16 ? 4 : V;
   using P = K1PlanP2<R, S, KIND, V, NT>;
@@ -197,10 +196,12 @@ cudaError_t launch_2d_s(const K1Launch& L, cudaStream_t stream) {
       if constexpr (sizeof(T) == 4 && R == 1 && KIND != KGRAD) {
         if (k1_v_override() == 2) return launch_2d_fixed<T, R, S, KIND, 2, 2>(L, stream);
         if (k1_impl_override() == 2) {
+          // 128-thread CTAs, 3 per SM: ptxas fits the pipeline in <= 170
+          // registers (12 warps per SM) without spilling
           if constexpr (S <= 4)
-            return launch_2d_p2<R, S, KIND, 4, 1>(L, stream);
+            return launch_2d_p2<R, S, KIND, 4, 128, 3>(L, stream);
           else
-            return launch_2d_p2<R, S, KIND, 2, 1>(L, stream);
+            return launch_2d_p2<R, S, KIND, 2, 128, 3>(L, stream);
         }
       }
       return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1>(L, stream);

@@ -56,7 +56,6 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
   using T = float;
   using P = K1PlanP2<R, S, KIND, V, NT>;
   constexpr int E = P::E, H = P::H, kRing = P::RING;
-  constexpr int VEC = (V * 4) >= 16 ? 4 : V;  // copy alignment unit (elements)
   const int tid = threadIdx.x, lane = tid & 31;
 
   // ---- geometry: rows shared, columns per strip ------------------------------
@@ -104,24 +103,37 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
       for (int k = 0; k < V; ++k) ap[u][e][k] = 0ull;
 
   // ---- prefetch: each lane reads back only what it copied (no barrier) -------
-  auto slot = [&](int row, int h) -> T* { return ring + ((row & (kRing - 1)) * 2 + h) * (NT * V) + tid * V; };
+  // Ring slot layout per lane: (A cell k, B cell k) interleaved, so the
+  // stage-0 row arrives as ready FFMA2 operand pairs (one LDS.64 per pair);
+  // with separate A and B vectors ptxas re-forms the pairs with IMAD.MOV on
+  // the FMA pipe for every FFMA2 that reads them. The price is 4-byte
+  // cp.async pieces (the lane's 4V bytes are L1-resident after the first).
+  auto slot = [&](int row) -> T* { return ring + (row & (kRing - 1)) * (NT * 2 * V) + tid * 2 * V; };
   auto issue = [&](int row) SO2DR_INLINE {
     if (row < hi0) {
-      const int64_t off = (int64_t)(row - sy0) * a.pitch;
-      const int cpb = row_cpb(a.in + off);  // warp-uniform
+      const T* src = a.in + (int64_t)(row - sy0) * a.pitch;
+      T* dst = slot(row);
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int v = 0; v < V; v += VEC)
-          issue_vec<T, VEC>(slot(row, h) + v, a.in + off + xt[h] + v, cpb, xt[h] + v, a.pitch);
+        for (int k = 0; k < V; ++k)
+          if (xt[h] + k >= 0 && xt[h] + k < a.pitch) cp_async<4>(dst + 2 * k + h, src + xt[h] + k);
     }
     cp_async_commit();
   };
+  // steady-state addressing off a running row offset (no 64-bit multiplies):
+  // load row = row0 + kRing - 1, store row = row0 - S(R+1)
+  int64_t off = (int64_t)(lo0 - sy0) * a.pitch;
+  const T* ldb = a.in + (int64_t)(kRing - 1) * a.pitch;
+  T* stb = a.out - (int64_t)(S * (R + 1)) * a.pitch;
   auto issue_fast = [&](int row) SO2DR_INLINE {
     if (row < hi0) {
-      const int64_t off = (int64_t)(row - sy0) * a.pitch;
+      const T* src = ldb + off;
+      T* dst = slot(row);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) issue_inrow<V * 4>(slot(row, h), a.in + off + xt[h]);
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < V; ++k) cp_async<4>(dst + 2 * k + h, src + xt[h] + k);
     }
     cp_async_commit();
   };
@@ -152,12 +164,12 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
       uint64_t op[V + 2 * R];
 #pragma unroll
       for (int k = 0; k < V; ++k) op[R + k] = in[k];
+      // 64-bit shuffles move a whole (A, B) pair: the two SHFLs land in an
+      // aligned register pair, ready as an FFMA2 operand
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        op[j] = pack2(__shfl_up_sync(0xffffffffu, lo_of(in[V - R + j]), 1),
-                      __shfl_up_sync(0xffffffffu, hi_of(in[V - R + j]), 1));
-        op[R + V + j] = pack2(__shfl_down_sync(0xffffffffu, lo_of(in[j]), 1),
-                              __shfl_down_sync(0xffffffffu, hi_of(in[j]), 1));
+        op[j] = __shfl_up_sync(0xffffffffu, in[V - R + j], 1);
+        op[R + V + j] = __shfl_down_sync(0xffffffffu, in[j], 1);
       }
 
       if (consume) {
@@ -196,8 +208,8 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
           }
         }
         if (u == S) {
-          T* da = a.out + (int64_t)(Erow - sy0) * a.pitch + xt[0];
-          T* db = a.out + (int64_t)(Erow - sy0) * a.pitch + xt[1];
+          T* da = stb + off + xt[0];  // row Erow = row0 - S(R+1)
+          T* db = stb + off + xt[1];
 #pragma unroll
           for (int k = 0; k < V; ++k) {
             if (smask[0] & (1u << k)) da[k] = lo_of(ap[u - 1][se][k]);
@@ -212,11 +224,11 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
     else
       issue(row0 + kRing - 1);
     cp_async_wait<kRing - 1>();
+    off += a.pitch;
     if (FAST || row0 < hi0) {
-      const T* sa = slot(row0, 0);
-      const T* sb = slot(row0, 1);
+      const uint64_t* sp = reinterpret_cast<const uint64_t*>(slot(row0));
 #pragma unroll
-      for (int k = 0; k < V; ++k) cp0[k] = pack2(sa[k], sb[k]);
+      for (int k = 0; k < V; ++k) cp0[k] = sp[k];
     }
   };
 

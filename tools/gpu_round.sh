@@ -21,14 +21,14 @@ for s in $steps; do
       SZ=32768 STENCILS=box2d1r,star2d1r KS=1,2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_bench.log 2>&1
       echo "k1 rc=$?" >> $OUT/summary.txt; cat $OUT/k1_bench.log >> $OUT/summary.txt ;;
     pipe)
-      timeout 1200 python tools/pipe_sweep.py > $OUT/pipe_sweep.log 2>&1
+      DS=${DS:-16,32,64} NS=${NS:-3} KS=${KS:-4,8} timeout 1200 python tools/pipe_sweep.py > $OUT/pipe_sweep.log 2>&1
       echo "pipe rc=$?" >> $OUT/summary.txt; cat $OUT/pipe_sweep.log >> $OUT/summary.txt ;;
     ncuk1)
-      for k in 4 8; do
-        timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_stencil2d -s 1 -c 1 -o $OUT/k1_incore_k$k -f \
-          python tools/k1_one.py $k 32768 box > $OUT/k1_incore_k$k.log 2>&1
-        echo "ncuk1 k=$k rc=$?" >> $OUT/summary.txt
-      done ;;
+      for impl in ${IMPLS:-pk p2}; do for k in ${NCU_KS:-4 8}; do
+        SO2DR_K1_IMPL=$impl timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_stencil2d -s 1 -c 1 \
+          -o $OUT/k1_${impl}_k$k -f python tools/k1_one.py $k 32768 box > $OUT/k1_${impl}_k$k.log 2>&1
+        echo "ncuk1 $impl k=$k rc=$?" >> $OUT/summary.txt
+      done; done ;;
     full)
       timeout 1500 python -m pytest tests/test_gpu_fullsize.py -x -q -m gpu --durations=0 > $OUT/pytest_fullsize.log 2>&1
       echo "fullsize rc=$?" >> $OUT/summary.txt; tail -12 $OUT/pytest_fullsize.log >> $OUT/summary.txt ;;
@@ -46,11 +46,49 @@ for s in $steps; do
       echo "pytest p2 rc=$?" >> $OUT/summary.txt; tail -2 $OUT/pytest_p2.log >> $OUT/summary.txt
       SO2DR_K1_IMPL=p2 SZ=32768 STENCILS=box2d1r,star2d1r KS=1,2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_bench_p2.log 2>&1
       echo "k1 p2 rc=$?" >> $OUT/summary.txt; cat $OUT/k1_bench_p2.log >> $OUT/summary.txt ;;
+    pcpipe)
+      timeout 600 python tools/pcie_pipe.py -v > $OUT/pcie_pipe.log 2>&1; echo "pcpipe rc=$?" >> $OUT/summary.txt
+      grep pattern $OUT/pcie_pipe.log >> $OUT/summary.txt ;;
+    diag)
+      timeout 300 python tools/pipe_profile.py 92160 16 8 3 > $OUT/pp_default.log 2>&1
+      SO2DR_DIAG_NO_K1=1 timeout 300 python tools/pipe_profile.py 92160 16 8 3 > $OUT/pp_nok1.log 2>&1
+      SO2DR_DIAG_NO_K1=1 SO2DR_DIAG_NO_D2D=1 timeout 300 python tools/pipe_profile.py 92160 16 8 3 > $OUT/pp_nok1_nod2d.log 2>&1
+      for f in pp_default pp_nok1 pp_nok1_nod2d; do echo $f >> $OUT/summary.txt; head -1 $OUT/$f.log >> $OUT/summary.txt; done ;;
+    fmapeak)
+      (cd tools/cu && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fma_peak fma_peak.cu && ./fma_peak) > $OUT/fma_peak.log 2>&1
+      echo "fmapeak rc=$?" >> $OUT/summary.txt; cat $OUT/fma_peak.log >> $OUT/summary.txt ;;
+    diag2)
+      SO2DR_DIAG_NO_K1=1 timeout 300 python tools/pipe_profile.py 92160 16 8 3 > $OUT/pp_nok1.log 2>&1
+      SO2DR_DIAG_NO_K1=1 HOST_ALLOC=torch timeout 300 python tools/pipe_profile.py 92160 16 8 3 > $OUT/pp_nok1_torch.log 2>&1
+      SO2DR_DIAG_NO_K1=1 SO2DR_HOST_ALLOC_DEFAULT=1 timeout 300 python tools/pipe_profile.py 92160 16 8 3 > $OUT/pp_nok1_dflt.log 2>&1
+      for f in pp_nok1 pp_nok1_torch pp_nok1_dflt; do echo $f >> $OUT/summary.txt; head -1 $OUT/$f.log >> $OUT/summary.txt; grep -E "c 5 (htod|dtoh)" $OUT/$f.log >> $OUT/summary.txt; done ;;
+    diag3)
+      for sp in 1 2 3; do
+        SO2DR_H2D_SPLIT=$sp SO2DR_DIAG_NO_K1=1 timeout 300 python tools/pipe_profile.py 92160 16 8 3 > $OUT/pp_split$sp.log 2>&1
+        echo split$sp >> $OUT/summary.txt; head -1 $OUT/pp_split$sp.log >> $OUT/summary.txt; grep -E "c 5 (htod|dtoh)" $OUT/pp_split$sp.log >> $OUT/summary.txt
+      done
+      for sp in 1 2; do
+        SO2DR_H2D_SPLIT=$sp timeout 300 python tools/pipe_profile.py 92160 64 4 3 > $OUT/pp_d64_split$sp.log 2>&1
+        echo d64 split$sp >> $OUT/summary.txt; head -1 $OUT/pp_d64_split$sp.log >> $OUT/summary.txt
+      done ;;
+    pcpipe2)
+      timeout 600 python tools/pcie_pipe2.py > $OUT/pcie_pipe2.log 2>&1; echo "pcpipe2 rc=$?" >> $OUT/summary.txt
+      cat $OUT/pcie_pipe2.log >> $OUT/summary.txt ;;
+    pcpipe3)
+      timeout 900 python tools/pcie_pipe3.py > $OUT/pcie_pipe3.log 2>&1; echo "pcpipe3 rc=$?" >> $OUT/summary.txt
+      cat $OUT/pcie_pipe3.log >> $OUT/summary.txt ;;
     ncu)
-      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
+      # launch list of one bench step (e2e leg): every launch with its device time
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
         python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-value-leg > $OUT/launches_bench.log 2>&1
       echo "ncu launches rc=$?" >> $OUT/summary.txt
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_stencil2d -s 20 -c 1 -o $OUT/k1_full -f \
+      # DRAM traffic of chunk 5's 16 K1 launches (steady state)
+      timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+        -k regex:k1_stencil2d -s 80 -c 16 --csv --log-file $OUT/k1_traffic.csv \
+        python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-value-leg > $OUT/k1_traffic.log 2>&1
+      echo "ncu traffic rc=$?" >> $OUT/summary.txt
+      # one full capture of a steady-state K1 launch
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_stencil2d -s 85 -c 1 -o $OUT/k1_full -f \
         python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-value-leg > $OUT/k1_full.log 2>&1
       echo "ncu full rc=$?" >> $OUT/summary.txt ;;
   esac

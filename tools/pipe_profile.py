@@ -15,8 +15,15 @@ d = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 k_on = int(sys.argv[3]) if len(sys.argv) > 3 else 8
 ns = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 eng = so2dr.Engine(0, 16 << 30)
-host = eng.host_array((sz + 2, sz + 2), np.float32)
-eng.init_grid(sz, 1, 42, out=host)
+if os.environ.get("HOST_ALLOC") == "torch":  # torch's pinned allocator instead of so2dr_host_alloc
+    import torch
+
+    host = torch.empty((sz + 2, sz + 2), dtype=torch.float32, pin_memory=True)
+    eng.init_grid(sz, 1, 42, out=host)
+else:
+    host = eng.host_array((sz + 2, sz + 2), np.float32)
+if not os.environ.get("HOST_ALLOC"):
+    eng.init_grid(sz, 1, 42, out=host)
 cfg = so2dr.RunConfig(sz=sz, r=1, d=d, s_tb=64, k_on=k_on, n_strm=ns, n=64)
 spec = so2dr.StencilSpec.box(1)
 eng.run("so2dr", host, spec, cfg, diag=False)  # warm
