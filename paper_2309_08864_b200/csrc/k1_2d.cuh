@@ -487,9 +487,16 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
                                            float (&ring)[K1Plan2D<float, R, S, KIND, V, NT>::RING][NT * V]) {
   using T = float;
   using P = K1Plan2D<T, R, S, KIND, V, NT>;
-  constexpr int E = P::E, H = P::H, VEC = P::VEC, CPB = P::CPB;
+  constexpr int E = P::E, H = P::H, VEC = P::VEC;
   constexpr int kRing = P::RING;
   constexpr int HV = V / 2;
+  // Accumulator ring of M = 2R+2 slots (output row y in slot y mod M), one more
+  // than the 2R+1 rows a consumed row touches. With 2R+1 slots the slot stage u
+  // reads (stage u-1's emission of the previous iteration) is the slot stage
+  // u-1 restarts in the same iteration, a register WAR inside the iteration;
+  // with the extra slot the read slot is not written in that iteration
+  // (measured +14% at k_on 1-2, +-2% at 4-8: profiles/r01_k1).
+  constexpr int M = E + 1;
   constexpr int NP = HV + 2 * R;  // operand pairs per consumed row
   static_assert(V % 2 == 0 && KIND != KGRAD, "packed path: box/star, even V");
   const int tid = threadIdx.x, lane = tid & 31;
@@ -524,7 +531,7 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
   const bool warp_ring = wc0 < a.ix0 || wc0 + 32 * V > a.ix1;
 
   // cell k of a packed row: pair k % HV, half k / HV
-  auto cell = [](const uint64_t (&p)[HV], int k) -> float {
+  auto cell = [](const uint64_t (&p)[HV], int k) SO2DR_INLINE -> float {
     float lo, hi;
     unpack2(p[k % HV], lo, hi);
     return k < HV ? lo : hi;
@@ -534,13 +541,13 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
   // which stage u+1 reads in the next iteration before stage u re-initialises
   // it (stages run in descending order). Only stage 0 has its own row.
   uint64_t cp0[HV];        // stage 0 (loaded) row, packed
-  uint64_t ap[S][E][HV];   // partial accumulators, packed
+  uint64_t ap[S][M][HV];   // partial accumulators, packed
 #pragma unroll
   for (int k = 0; k < HV; ++k) cp0[k] = 0ull;
 #pragma unroll
   for (int u = 0; u < S; ++u)
 #pragma unroll
-    for (int e = 0; e < E; ++e)
+    for (int e = 0; e < M; ++e)
 #pragma unroll
       for (int k = 0; k < HV; ++k) ap[u][e][k] = 0ull;
 
@@ -586,7 +593,9 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
       // the consumed row: stage u-1's emission of the previous iteration
       uint64_t in[HV];
 #pragma unroll
-      for (int k = 0; k < HV; ++k) in[k] = (u == 1) ? cp0[k] : ap[u >= 2 ? u - 2 : 0][PH][k];
+      // stage u-1 emitted it last iteration into slot (PH - 1 - 2R) mod M
+      constexpr int rd_slot = (PH - 1 - 2 * R + 2 * M) % M;
+      for (int k = 0; k < HV; ++k) in[k] = (u == 1) ? cp0[k] : ap[u >= 2 ? u - 2 : 0][rd_slot][k];
       // halo values (lanes 0/31 get their own: strip-edge garbage, never output)
       float hl[R], hr[R];
 #pragma unroll
@@ -595,7 +604,7 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
         hr[j] = __shfl_down_sync(0xffffffffu, cell(in, j), 1);
       }
       // s_i: i < R halo-left, R <= i < R+V own cell i-R, else halo-right
-      auto sval = [&](int i) -> float {
+      auto sval = [&](int i) SO2DR_INLINE -> float {
         if (i < R) return hl[i];
         if (i < R + V) return cell(in, i - R);
         return hr[i - R - V];
@@ -608,7 +617,7 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
 #pragma unroll
         for (int m = 0; m < E; ++m) {
           const int dy = m - R;
-          const int sl = (PH - m + 2 * E) % E;
+          const int sl = (PH - m + 2 * M) % M;
 #pragma unroll
           for (int k = 0; k < HV; ++k) {
             uint64_t x = (m == 0) ? 0ull : ap[u - 1][sl][k];
@@ -626,7 +635,7 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
         }
       }
       if (emit) {
-        constexpr int se = (PH - 2 * R + 2 * E) % E;
+        constexpr int se = (PH - 2 * R + 2 * M) % M;
         uint64_t outp[HV];
 #pragma unroll
         for (int k = 0; k < HV; ++k) outp[k] = ap[u - 1][se][k];
@@ -681,16 +690,16 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
         ((it < stop ? (body(std::integral_constant<int, Ps>{}, std::false_type{}, it), ++it, void())
                     : void()),
          ...);
-      }(std::make_integer_sequence<int, E>{});
+      }(std::make_integer_sequence<int, M>{});
     }
   };
-  const int fl = (f_lo + E - 1) / E * E;
-  if (f_hi - fl >= E) {
+  const int fl = (f_lo + M - 1) / M * M;
+  if (f_hi - fl >= M) {
     run_general(fl);
-    while (it + E <= f_hi) {
+    while (it + M <= f_hi) {
       [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
         ((body(std::integral_constant<int, Ps>{}, std::true_type{}, it), ++it), ...);
-      }(std::make_integer_sequence<int, E>{});
+      }(std::make_integer_sequence<int, M>{});
     }
   }
   run_general(n_iter);

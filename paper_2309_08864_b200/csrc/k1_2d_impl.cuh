@@ -51,6 +51,17 @@ inline int k1_impl_override() {
   return v;
 }
 
+// Work items per resident warp (row segments x strips). Default 8; shorter
+// segments balance the tail, longer ones amortise the R*S warm-up rows.
+// SO2DR_K1_IPW=n overrides (experiments).
+inline int k1_items_per_warp() {
+  static int v = [] {
+    const char* s = std::getenv("SO2DR_K1_IPW");
+    return s ? std::max(1, std::atoi(s)) : 8;
+  }();
+  return v;
+}
+
 template <typename T, int R, int S, int KIND, int V, int MINB>
 cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   constexpr int NT = kThreads2D;
@@ -113,7 +124,7 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   const int resident_warps = sms * occ * NW;
   const int min_seg = std::max(48, 6 * (H + S * (R + 1)));
   const int max_ns = std::max(1, height / min_seg);
-  int ns = std::max(1, (8 * resident_warps + a.warps_x - 1) / a.warps_x);
+  int ns = std::max(1, (k1_items_per_warp() * resident_warps + a.warps_x - 1) / a.warps_x);
   ns = std::min(ns, max_ns);
   a.seg = (height + ns - 1) / ns;
   a.nseg = (height + a.seg - 1) / a.seg;
@@ -175,7 +186,7 @@ cudaError_t launch_2d_p2(const K1Launch& L, cudaStream_t stream) {
   const int resident_warps = sms * occ * NW;
   const int min_seg = std::max(48, 6 * (H + S * (R + 1)));
   const int max_ns = std::max(1, height / min_seg);
-  int ns = std::max(1, (8 * resident_warps + np - 1) / np);
+  int ns = std::max(1, (k1_items_per_warp() * resident_warps + np - 1) / np);
   ns = std::min(ns, max_ns);
   a.seg = (height + ns - 1) / ns;
   a.nseg = (height + a.seg - 1) / a.seg;
@@ -195,13 +206,13 @@ cudaError_t launch_2d_s(const K1Launch& L, cudaStream_t stream) {
     if (L.steps == S) {
       if constexpr (sizeof(T) == 4 && R == 1 && KIND != KGRAD) {
         if (k1_v_override() == 2) return launch_2d_fixed<T, R, S, KIND, 2, 2>(L, stream);
-        if (k1_impl_override() == 2) {
-          // 128-thread CTAs, 3 per SM: ptxas fits the pipeline in <= 170
-          // registers (12 warps per SM) without spilling
-          if constexpr (S <= 4)
-            return launch_2d_p2<R, S, KIND, 4, 128, 3>(L, stream);
-          else
-            return launch_2d_p2<R, S, KIND, 2, 128, 3>(L, stream);
+        // Paired-strip kernel for S = 3..4 (measured +3% over pk at S = 4 in-core,
+        // profiles/r01_k1; pk wins below, and at S > 4 p2 needs V = 2 and spills).
+        // 128-thread CTAs, 3 per SM: <= 170 registers, no spill.
+        // SO2DR_K1_IMPL=pk|p2 forces one (p2 only where it exists).
+        if constexpr (S >= 3 && S <= 4) {
+          const int impl = k1_impl_override();
+          if (impl == 2 || impl == 0) return launch_2d_p2<R, S, KIND, 4, 128, 3>(L, stream);
         }
       }
       return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1>(L, stream);

@@ -32,7 +32,7 @@ namespace so2dr_dev {
 template <int R, int S, int KIND, int V, int NT>
 struct K1PlanP2 {
   static constexpr int RING = 8;  // prefetch ring depth (rows)
-  // dynamic shared memory: ring[RING][2][NT * V] floats (64 KB at V = 4)
+  // dynamic shared memory: ring[RING][2][NT * V] floats
   static constexpr size_t SMEM = sizeof(float) * RING * 2 * NT * V;
   static constexpr int E = 2 * R + 1;
   static constexpr int H = R * S;
@@ -56,6 +56,7 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
   using T = float;
   using P = K1PlanP2<R, S, KIND, V, NT>;
   constexpr int E = P::E, H = P::H, kRing = P::RING;
+  constexpr int VEC = (V * 4) % 16 == 0 ? 4 : (V * 4) % 8 == 0 ? 2 : 1;  // cp.async unit (elements)
   const int tid = threadIdx.x, lane = tid & 31;
 
   // ---- geometry: rows shared, columns per strip ------------------------------
@@ -91,10 +92,10 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
     hi[u] = min(OY1 + R * (S - u), sy1);
   }
 
-  uint64_t cp0[V];       // stage-0 (loaded) row: (A cell k, B cell k)
+  float c0a[V], c0b[V];  // stage-0 (loaded) row: A cells, B cells
   uint64_t ap[S][E][V];  // partial accumulators; stage u's emitted row stays in its slot
 #pragma unroll
-  for (int k = 0; k < V; ++k) cp0[k] = 0ull;
+  for (int k = 0; k < V; ++k) c0a[k] = c0b[k] = 0.f;
 #pragma unroll
   for (int u = 0; u < S; ++u)
 #pragma unroll
@@ -103,21 +104,21 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
       for (int k = 0; k < V; ++k) ap[u][e][k] = 0ull;
 
   // ---- prefetch: each lane reads back only what it copied (no barrier) -------
-  // Ring slot layout per lane: (A cell k, B cell k) interleaved, so the
-  // stage-0 row arrives as ready FFMA2 operand pairs (one LDS.64 per pair);
-  // with separate A and B vectors ptxas re-forms the pairs with IMAD.MOV on
-  // the FMA pipe for every FFMA2 that reads them. The price is 4-byte
-  // cp.async pieces (the lane's 4V bytes are L1-resident after the first).
-  auto slot = [&](int row) -> T* { return ring + (row & (kRing - 1)) * (NT * 2 * V) + tid * 2 * V; };
+  // Ring slot per lane: A's V cells then B's V cells, each copied with the
+  // widest cp.async the row alignment allows (an interleaved (A_k, B_k) layout
+  // needs 4-byte copies: 4x the L1 wavefronts, MIO-throttled, profiles/r01_k1).
+  // Stage 1 therefore consumes the loaded row as two scalar vectors (FFMA into
+  // the halves of its pair accumulators); stages 2..S run on pairs (FFMA2).
+  auto slot = [&](int row, int h) -> T* { return ring + ((row & (kRing - 1)) * 2 + h) * (NT * V) + tid * V; };
   auto issue = [&](int row) SO2DR_INLINE {
     if (row < hi0) {
-      const T* src = a.in + (int64_t)(row - sy0) * a.pitch;
-      T* dst = slot(row);
+      const int64_t roff = (int64_t)(row - sy0) * a.pitch;
+      const int cpb = row_cpb(a.in + roff);  // warp-uniform
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int k = 0; k < V; ++k)
-          if (xt[h] + k >= 0 && xt[h] + k < a.pitch) cp_async<4>(dst + 2 * k + h, src + xt[h] + k);
+        for (int v = 0; v < V; v += VEC)
+          issue_vec<T, VEC>(slot(row, h) + v, a.in + roff + xt[h] + v, cpb, xt[h] + v, a.pitch);
     }
     cp_async_commit();
   };
@@ -128,12 +129,8 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
   T* stb = a.out - (int64_t)(S * (R + 1)) * a.pitch;
   auto issue_fast = [&](int row) SO2DR_INLINE {
     if (row < hi0) {
-      const T* src = ldb + off;
-      T* dst = slot(row);
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int k = 0; k < V; ++k) cp_async<4>(dst + 2 * k + h, src + xt[h] + k);
+      for (int h = 0; h < 2; ++h) issue_inrow<V * 4>(slot(row, h), ldb + off + xt[h]);
     }
     cp_async_commit();
   };
@@ -156,9 +153,58 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
       const bool consume = FAST || (A >= lo[u - 1] && A < hi[u - 1]);
       const bool emit = FAST || (Erow >= lo[u] && Erow < hi[u]);
 
+      if (u == 1) {
+        // stage 1: scalar FFMAs on the loaded A / B vectors into the halves of
+        // the pair accumulators (same canonical chain per point)
+        float ha[R + V + R], hb[R + V + R];
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          ha[R + k] = c0a[k];
+          hb[R + k] = c0b[k];
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          ha[j] = __shfl_up_sync(0xffffffffu, c0a[V - R + j], 1);
+          hb[j] = __shfl_up_sync(0xffffffffu, c0b[V - R + j], 1);
+          ha[R + V + j] = __shfl_down_sync(0xffffffffu, c0a[j], 1);
+          hb[R + V + j] = __shfl_down_sync(0xffffffffu, c0b[j], 1);
+        }
+        if (consume) {
+#pragma unroll
+          for (int m = 0; m < E; ++m) {
+            const int dy = m - R;
+            const int sl = (PH - m + 2 * E) % E;
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+              float xa = (m == 0) ? 0.f : lo_of(ap[0][sl][k]);
+              float xb = (m == 0) ? 0.f : hi_of(ap[0][sl][k]);
+              if constexpr (KIND == KBOX) {
+#pragma unroll
+                for (int dx = -R; dx <= R; ++dx) {
+                  const float w = a.w[(dy + R) * E + dx + R];
+                  xa = __fmaf_rn(w, ha[R + k + dx], xa);
+                  xb = __fmaf_rn(w, hb[R + k + dx], xb);
+                }
+              } else if (dy != 0) {
+                const float w = a.w[(dy + R) * E + R];
+                xa = __fmaf_rn(w, ha[R + k], xa);
+                xb = __fmaf_rn(w, hb[R + k], xb);
+              } else {
+#pragma unroll
+                for (int dx = -R; dx <= R; ++dx) {
+                  const float w = a.w[R * E + dx + R];
+                  xa = __fmaf_rn(w, ha[R + k + dx], xa);
+                  xb = __fmaf_rn(w, hb[R + k + dx], xb);
+                }
+              }
+              ap[0][sl][k] = pack2(xa, xb);
+            }
+          }
+        }
+      } else {
       uint64_t in[V];
 #pragma unroll
-      for (int k = 0; k < V; ++k) in[k] = (u == 1) ? cp0[k] : ap[u >= 2 ? u - 2 : 0][PH][k];
+      for (int k = 0; k < V; ++k) in[k] = ap[u >= 2 ? u - 2 : 0][PH][k];
       // operand pairs: op[i] = (A s_i, B s_i), s_i = cell i-R (halo for i < R or i >= R+V);
       // lanes 0 / 31 receive their own values: strip-edge garbage, never stored
       uint64_t op[V + 2 * R];
@@ -193,6 +239,7 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
           }
         }
       }
+      }
       if (emit) {
         constexpr int se = (PH - 2 * R + 2 * E) % E;  // slot of row A - R
         if constexpr (!FAST) {
@@ -226,9 +273,13 @@ __device__ __forceinline__ void k1_item_p2(const K1Args2D<float>& a, int q, int 
     cp_async_wait<kRing - 1>();
     off += a.pitch;
     if (FAST || row0 < hi0) {
-      const uint64_t* sp = reinterpret_cast<const uint64_t*>(slot(row0));
+      const T* sa = slot(row0, 0);
+      const T* sb = slot(row0, 1);
 #pragma unroll
-      for (int k = 0; k < V; ++k) cp0[k] = sp[k];
+      for (int k = 0; k < V; ++k) {
+        c0a[k] = sa[k];
+        c0b[k] = sb[k];
+      }
     }
   };
 

@@ -77,6 +77,11 @@ for s in $steps; do
     pcpipe3)
       timeout 900 python tools/pcie_pipe3.py > $OUT/pcie_pipe3.log 2>&1; echo "pcpipe3 rc=$?" >> $OUT/summary.txt
       cat $OUT/pcie_pipe3.log >> $OUT/summary.txt ;;
+    ipw)
+      for ipw in 4 8 16 32; do for impl in pk p2; do
+        SO2DR_K1_IPW=$ipw SO2DR_K1_IMPL=$impl SZ=32768 STENCILS=box2d1r KS=2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_ipw${ipw}_${impl}.log 2>&1
+        echo "ipw=$ipw impl=$impl" >> $OUT/summary.txt; cat $OUT/k1_ipw${ipw}_${impl}.log >> $OUT/summary.txt
+      done; done ;;
     ncu)
       # launch list of one bench step (e2e leg): every launch with its device time
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
