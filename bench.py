@@ -74,15 +74,16 @@ class ClockSampler:
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 200):
         self.index = index
+        self.period_ms = period_ms
         self.rows = []
         self.proc = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -230,6 +231,10 @@ def main():
     ap.add_argument("--k-on", type=int, default=K_ON)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-value-leg", action="store_true")
+    ap.add_argument("--pcie-probe-before", action="store_true",
+                    help="measure the PCIe roof before the timed e2e leg (default: right after it; the torch "
+                         "probe's pinned buffers cost the e2e leg ~1.5%% when taken before)")
+    ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period during the timed e2e leg")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
@@ -328,10 +333,12 @@ def main():
     t_reg = time.perf_counter() - t0
     eng.init_rows(sz, R, 42, lo, hi, host)
     connect()
-    pc = pcie_probe(torch, dev) if rank == 0 else {}
-    with ClockSampler(dev_index) as clk:
+    pc = pcie_probe(torch, dev) if rank == 0 and args.pcie_probe_before else {}
+    with ClockSampler(dev_index, args.clock_ms) as clk:
         e2e_res = leg(host, args.steps, args.warmup)
     clocks = clk.summary()
+    if rank == 0 and not args.pcie_probe_before:
+        pc = pcie_probe(torch, dev)
 
     if rank != 0:
         if world > 1:

@@ -206,13 +206,13 @@ cudaError_t launch_2d_s(const K1Launch& L, cudaStream_t stream) {
     if (L.steps == S) {
       if constexpr (sizeof(T) == 4 && R == 1 && KIND != KGRAD) {
         if (k1_v_override() == 2) return launch_2d_fixed<T, R, S, KIND, 2, 2>(L, stream);
-        // Paired-strip kernel for S = 3..4 (measured +3% over pk at S = 4 in-core,
-        // profiles/r01_k1; pk wins below, and at S > 4 p2 needs V = 2 and spills).
-        // 128-thread CTAs, 3 per SM: <= 170 registers, no spill.
-        // SO2DR_K1_IMPL=pk|p2 forces one (p2 only where it exists).
+        // Paired-strip kernel (SO2DR_K1_IMPL=p2; S = 3..4 only: at S > 4 it needs
+        // V = 2 and spills). In-core it is within noise of pk (+-3% at S = 4,
+        // profiles/r01_k1); inside the bench pipeline (d=64, ~1500-row
+        // launches) it was 20% slower per launch (0.54 vs 0.45 ms), so pk stays
+        // the default. 128-thread CTAs, 3 per SM: <= 170 registers, no spill.
         if constexpr (S >= 3 && S <= 4) {
-          const int impl = k1_impl_override();
-          if (impl == 2 || impl == 0) return launch_2d_p2<R, S, KIND, 4, 128, 3>(L, stream);
+          if (k1_impl_override() == 2) return launch_2d_p2<R, S, KIND, 4, 128, 3>(L, stream);
         }
       }
       return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1>(L, stream);

@@ -82,6 +82,23 @@ for s in $steps; do
         SO2DR_K1_IPW=$ipw SO2DR_K1_IMPL=$impl SZ=32768 STENCILS=box2d1r KS=2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_ipw${ipw}_${impl}.log 2>&1
         echo "ipw=$ipw impl=$impl" >> $OUT/summary.txt; cat $OUT/k1_ipw${ipw}_${impl}.log >> $OUT/summary.txt
       done; done ;;
+    allocvar)
+      timeout 1200 python tools/alloc_var.py > $OUT/alloc_var.log 2>&1; echo "allocvar rc=$?" >> $OUT/summary.txt
+      cat $OUT/alloc_var.log >> $OUT/summary.txt ;;
+    clockab)
+      for cms in 200 1000 200 1000; do
+        timeout 900 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-value-leg --clock-ms $cms > $OUT/bench_c$cms.log 2>&1
+        echo "clock_ms=$cms" >> $OUT/summary.txt
+        tail -1 $OUT/bench_c$cms.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['e2e']['value'], d['ms_per_step'], d['clocks'])" >> $OUT/summary.txt
+      done ;;
+    probeab)
+      for v in before after before after; do
+        flag=""; [ $v = after ] && flag="--pcie-probe-after"
+        timeout 900 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-value-leg $flag > $OUT/bench_p$v.log 2>&1
+        echo "probe=$v" >> $OUT/summary.txt
+        tail -1 $OUT/bench_p$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['e2e']['value'], d['ms_per_step'], d['binding_roofline']['pcie_measured'])" >> $OUT/summary.txt
+      done
+      timeout 600 python tools/alloc_var.py > $OUT/alloc_var.log 2>&1; grep alloc $OUT/alloc_var.log >> $OUT/summary.txt ;;
     ncu)
       # launch list of one bench step (e2e leg): every launch with its device time
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
