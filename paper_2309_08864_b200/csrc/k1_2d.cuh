@@ -205,7 +205,7 @@ struct K1Plan2D {
 
 // One work item = (strip wx, row segment sg) processed by one warp; `ring` is
 // the calling CTA's shared ring (each lane uses its own slots only).
-template <typename T, int R, int S, int KIND, int V, int NT>
+template <typename T, int R, int S, int KIND, int V, int NT, bool SCALAR = false>
 __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
                                         T (&ring)[K1Plan2D<T, R, S, KIND, V, NT>::RING][NT * V]) {
   using P = K1Plan2D<T, R, S, KIND, V, NT>;
@@ -346,7 +346,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
           for (int m = 0; m < E; ++m) {
             const int dy = m - R;                 // A contributes at dy to row A-dy
             const int sl = (PH - m + 2 * E) % E;  // slot of output row A+R-m
-            if constexpr (sizeof(T) == 4 && V % 2 == 0) {
+            if constexpr (sizeof(T) == 4 && V % 2 == 0 && !SCALAR) {
               // fp32: two cells per FFMA2 (fma.rn.f32x2, sm_100a); each half is
               // an IEEE fma with round-to-nearest, so the chain is bit-identical
               // to the scalar __fmaf_rn chain. Cells are paired (k, k+V/2), not
@@ -729,7 +729,7 @@ __device__ __forceinline__ void k1_item_coords(const K1Args2D<T>& a, int item, i
 // Persistent warps with dynamic work distribution: every warp of a
 // one-wave grid fetches (strip, segment) items from an atomic counter, so the
 // SMs stay busy until the last item (no partial last wave).
-template <typename T, int R, int S, int KIND, int V, int NT, int MINB>
+template <typename T, int R, int S, int KIND, int V, int NT, int MINB, bool SCALAR = false>
 __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
   __shared__ __align__(16) T ring[K1Plan2D<T, R, S, KIND, V, NT>::RING][NT * V];
   const int lane = threadIdx.x & 31;
@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
     if (item >= total) break;
     int wx, sg;
     k1_item_coords(a, item, wx, sg);
-    k1_item<T, R, S, KIND, V, NT>(a, wx, sg, ring);
+    k1_item<T, R, S, KIND, V, NT, SCALAR>(a, wx, sg, ring);
   }
 }
 

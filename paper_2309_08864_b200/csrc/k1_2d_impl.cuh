@@ -62,7 +62,8 @@ inline int k1_items_per_warp() {
   return v;
 }
 
-template <typename T, int R, int S, int KIND, int V, int MINB>
+template <typename T, int R, int S, int KIND, int V, int MINB,
+          bool PACK = std::is_same_v<T, float> && KIND != KGRAD && V % 2 == 0>
 cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   constexpr int NT = kThreads2D;
   constexpr int H = R * S;
@@ -108,12 +109,12 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   // One wave of persistent CTAs; warps pull (strip, segment) items from a
   // counter. Segments: ~8 items per resident warp for load balance, but each
   // at least 6x its warm-up (R*S rows + S*(R+1) pipeline fill) long.
-  constexpr bool packed = std::is_same_v<T, float> && KIND != KGRAD && V % 2 == 0;
+  constexpr bool packed = PACK;
   auto kern = [] {
     if constexpr (packed)
       return k1_stencil2d_pk<R, S, KIND, V, NT, MINB>;
     else
-      return k1_stencil2d<T, R, S, KIND, V, NT, MINB>;
+      return k1_stencil2d<T, R, S, KIND, V, NT, MINB, std::is_same_v<T, float> && KIND != KGRAD>;
   }();
   static int occ = 0;
   if (occ == 0) {
@@ -214,8 +215,24 @@ cudaError_t launch_2d_s(const K1Launch& L, cudaStream_t stream) {
         if constexpr (S >= 3 && S <= 4) {
           if (k1_impl_override() == 2) return launch_2d_p2<R, S, KIND, 4, 128, 3>(L, stream);
         }
+
       }
-      return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1>(L, stream);
+      // fp32 box/star: the scalar-FFMA pipeline (k1_item) is the default. FFMA
+      // reaches the same FMA rate as FFMA2 on this part (36.4 vs 36.9 TFMA/s,
+      // profiles/r01_pcie/fma_peak.jsonl), and without register pairs ptxas
+      // needs no IMAD.MOVs to assemble operands: +11-19% over the packed
+      // kernel in-core (profiles/r01_k1/scalar_vs_pk.txt). SO2DR_K1_IMPL=pk
+      // selects the packed FFMA2 kernel.
+      // (the packed kernel is built for r <= 2 only: at r >= 3 its 2r+2-slot
+      // ring outgrows the register file)
+      if constexpr (sizeof(T) == 4 && KIND != KGRAD && R >= 3) {
+        return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1, false>(L, stream);
+      } else {
+        if constexpr (sizeof(T) == 4 && KIND != KGRAD) {
+          if (k1_impl_override() != 1) return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1, false>(L, stream);
+        }
+        return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1>(L, stream);
+      }
     }
     return launch_2d_s<T, R, KIND, S + 1>(L, stream);
   }

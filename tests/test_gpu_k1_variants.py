@@ -1,6 +1,7 @@
-"""The experimental paired-strip K1 (k1_2d_p2.cuh, selected with
-SO2DR_K1_IMPL=p2 at S = 3..4) must stay bit-exact with the oracle like the
-default kernel. Run in a subprocess: the variant is chosen once per process."""
+"""Every fp32 K1 variant must stay bit-exact with the oracle: the default
+scalar-FFMA pipeline, the packed FFMA2 kernel (SO2DR_K1_IMPL=pk) and the
+paired-strip kernel (SO2DR_K1_IMPL=p2, S = 3..4). Run in a subprocess: the
+variant is chosen once per process."""
 import os
 import subprocess
 import sys
@@ -32,9 +33,12 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("impl", ["p2", "pk"])
+@pytest.mark.parametrize("impl", ["p2", "pk", "default"])
 def test_k1_variant_bit_exact(impl):
-    env = dict(os.environ, SO2DR_K1_IMPL=impl)
+    env = dict(os.environ)
+    env.pop("SO2DR_K1_IMPL", None)
+    if impl != "default":
+        env["SO2DR_K1_IMPL"] = impl
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

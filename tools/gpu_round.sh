@@ -18,7 +18,7 @@ for s in $steps; do
       timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > $OUT/bench_ref.log 2>&1; echo "ref rc=$?" >> $OUT/summary.txt
       tail -1 $OUT/bench_ref.log >> $OUT/summary.txt ;;
     k1)
-      SZ=32768 STENCILS=box2d1r,star2d1r KS=1,2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_bench.log 2>&1
+      SZ=32768 STENCILS=${STENCILS:-box2d1r,star2d1r} KS=${KS:-1,2,4,8} timeout 900 python tools/k1_bench.py > $OUT/k1_bench.log 2>&1
       echo "k1 rc=$?" >> $OUT/summary.txt; cat $OUT/k1_bench.log >> $OUT/summary.txt ;;
     pipe)
       DS=${DS:-16,32,64} NS=${NS:-3} KS=${KS:-4,8} timeout 1200 python tools/pipe_sweep.py > $OUT/pipe_sweep.log 2>&1
@@ -99,6 +99,18 @@ for s in $steps; do
         tail -1 $OUT/bench_p$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['e2e']['value'], d['ms_per_step'], d['binding_roofline']['pcie_measured'])" >> $OUT/summary.txt
       done
       timeout 600 python tools/alloc_var.py > $OUT/alloc_var.log 2>&1; grep alloc $OUT/alloc_var.log >> $OUT/summary.txt ;;
+    ipwbench)
+      for ipw in 3 4 6 8 12; do
+        SO2DR_K1_IPW=$ipw timeout 900 python bench.py --steps 3 --warmup 2 --no-cpu-baseline > $OUT/bench_ipw$ipw.log 2>&1
+        echo "ipw=$ipw" >> $OUT/summary.txt
+        tail -1 $OUT/bench_ipw$ipw.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), 'K1 ms', round(d['roofline']['avg_launch_ms'],4), 'frac', round(d['roofline']['frac'],3))" >> $OUT/summary.txt
+      done ;;
+    scalar)
+      for impl in pk scalar; do
+        SO2DR_K1_IMPL=$impl SZ=32768 STENCILS=box2d1r,star2d1r KS=2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_$impl.log 2>&1
+        echo "impl=$impl" >> $OUT/summary.txt; cat $OUT/k1_$impl.log >> $OUT/summary.txt
+      done
+      SO2DR_K1_IMPL=scalar timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q > $OUT/pytest_scalar.log 2>&1; echo "pytest scalar rc=$?" >> $OUT/summary.txt ;;
     ncu)
       # launch list of one bench step (e2e leg): every launch with its device time
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
