@@ -403,7 +403,7 @@ uint64_t device_footprint(const so2dr::RunConfig& cfg, const Geo& g, int n_strm)
 
 // Copy `n` units between a device field (pitch g.pitch) and the grid (host or
 // device, dense rows of g.p cells). Uses the 2D copy engine path.
-constexpr uintptr_t kPcieAlign = 128;  // bytes; see copy_units
+constexpr uintptr_t kPcieAlign = 64 << 10;  // bytes; see copy_units
 
 static void copy_units(const Geo& g, void* dst, int64_t dst_pitch, const void* src,
                        int64_t src_pitch, int64_t n, cudaStream_t s,
@@ -411,10 +411,12 @@ static void copy_units(const Geo& g, void* dst, int64_t dst_pitch, const void* s
   if (n <= 0) return;
   if (dst_pitch == g.p && src_pitch == g.p) {  // dense on both sides: one contiguous copy
     const size_t bytes = static_cast<size_t>(n * g.unit_rows * g.p * g.elem);
-    // PCIe copies start at a 128-byte aligned HOST address: a copy whose host
-    // side starts off a 128-byte boundary runs D2H at ~42 instead of ~50 GB/s
-    // in duplex (profiles/r01_pcie). Dense rows of the grid start at any
-    // 8-byte offset, so the unaligned head (< 128 B) goes as its own copy.
+    // PCIe copies start at a 64 KiB aligned HOST address; the unaligned head
+    // (< 64 KiB) goes as its own copy. Dense rows of the grid start at any
+    // 8-byte offset, and the host-side start alignment sets the duplex rates
+    // (copy-only model of this pipeline, profiles/r01_pcie): 8-byte aligned
+    // 52.7/41.6 GB/s (H2D/D2H), 128 B 40.4/50.5, 512 B 46.4/50.4, 64 KiB
+    // 47.8/50.5 -- 866 -> 743 ms per 34 GB round trip.
     const void* host = kind == cudaMemcpyHostToDevice ? src : kind == cudaMemcpyDeviceToHost ? dst : nullptr;
     size_t head = host ? (kPcieAlign - (reinterpret_cast<uintptr_t>(host) & (kPcieAlign - 1))) & (kPcieAlign - 1) : 0;
     if (head >= bytes) head = 0;

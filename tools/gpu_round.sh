@@ -111,6 +111,16 @@ for s in $steps; do
         echo "impl=$impl" >> $OUT/summary.txt; cat $OUT/k1_$impl.log >> $OUT/summary.txt
       done
       SO2DR_K1_IMPL=scalar timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q > $OUT/pytest_scalar.log 2>&1; echo "pytest scalar rc=$?" >> $OUT/summary.txt ;;
+    robust)
+      DS=32,64,128 NS=3,4,6 KS=4 timeout 1500 python tools/pipe_sweep.py > $OUT/pipe_sweep_robust.log 2>&1
+      echo "robust rc=$?" >> $OUT/summary.txt; cat $OUT/pipe_sweep_robust.log >> $OUT/summary.txt
+      timeout 300 python tools/pipe_profile.py 92160 64 4 3 > $OUT/pp_d64.log 2>&1
+      head -1 $OUT/pp_d64.log >> $OUT/summary.txt; grep -E "c(20|21|22) (htod|dtoh)" $OUT/pp_d64.log >> $OUT/summary.txt ;;
+    robust2)
+      DS=64,128,192 NS=3 KS=4,8 timeout 1500 python tools/pipe_sweep.py > $OUT/pipe_sweep_robust2.log 2>&1
+      echo "robust2 rc=$?" >> $OUT/summary.txt; cat $OUT/pipe_sweep_robust2.log >> $OUT/summary.txt
+      timeout 300 python tools/pipe_profile.py 92160 64 4 3 > $OUT/pp_d64.log 2>&1
+      head -1 $OUT/pp_d64.log >> $OUT/summary.txt; grep -E "c(20|21|22) (htod|dtoh)" $OUT/pp_d64.log >> $OUT/summary.txt ;;
     ncu)
       # launch list of one bench step (e2e leg): every launch with its device time
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \

@@ -23,9 +23,9 @@ def rows_h2d(i):
     return lo, hi
 
 
-def copy(dst, src, nbytes, head_split, host_addr, tail_split=False):
-    head = (128 - host_addr % 128) % 128 if head_split else 0
-    tail = (host_addr + nbytes) % 128 if tail_split else 0
+def copy(dst, src, nbytes, head_split, host_addr, tail_split=False, align=128):
+    head = (align - host_addr % align) % align if head_split else 0
+    tail = (host_addr + nbytes) % align if tail_split else 0
     if head:
         dst[:head].copy_(src[:head], non_blocking=True)
     dst[head:nbytes - tail].copy_(src[head:nbytes - tail], non_blocking=True)
@@ -33,7 +33,7 @@ def copy(dst, src, nbytes, head_split, host_addr, tail_split=False):
         dst[nbytes - tail:nbytes].copy_(src[nbytes - tail:nbytes], non_blocking=True)
 
 
-def run(head_split=True, congruent=True, tail_h=False, tail_d=False):
+def run(head_split=True, congruent=True, tail_h=False, tail_d=False, align=128):
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t0.record()
@@ -53,7 +53,7 @@ def run(head_split=True, congruent=True, tail_h=False, tail_d=False):
                 s_h.wait_event(done[i - 3])
             a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            copy(dv[(lo - wlo) * RB:], hb, (hi - lo) * RB, head_split, hb.data_ptr(), tail_h)
+            copy(dv[(lo - wlo) * RB:], hb, (hi - lo) * RB, head_split, hb.data_ptr(), tail_h, align)
             z.record()
             ev[("h", i)] = (a, z, (hi - lo) * RB)
         with torch.cuda.stream(s_d):
@@ -62,7 +62,7 @@ def run(head_split=True, congruent=True, tail_h=False, tail_d=False):
             a2.record()
             clo, chi = fence[i], fence[i + 1]
             hd = host[clo * RB:chi * RB]
-            copy(hd, dv[(clo - wlo) * RB:], (chi - clo) * RB, head_split, hd.data_ptr(), tail_d)
+            copy(hd, dv[(clo - wlo) * RB:], (chi - clo) * RB, head_split, hd.data_ptr(), tail_d, align)
             z2.record()
             done[i] = z2
             ev[("d", i)] = (a2, z2, (chi - clo) * RB)
@@ -76,8 +76,9 @@ def run(head_split=True, congruent=True, tail_h=False, tail_d=False):
 
 run()
 for trial in range(2):
-    for name, kw in (("engine_geometry", {}), ("tail_h2d", {"tail_h": True}), ("tail_d2h", {"tail_d": True}),
-                     ("tail_both", {"tail_h": True, "tail_d": True})):
+    for name, kw in (("align128", {}), ("align512", {"align": 512}), ("align4096", {"align": 4096}),
+                     ("align4096_tails", {"align": 4096, "tail_h": True, "tail_d": True}),
+                     ("align65536", {"align": 65536})):
         t, h, d = run(**kw)
         print(json.dumps({"trial": trial, "pattern": name, "total_ms": round(t, 1), "steady_h2d_GBps": round(h, 1),
                           "steady_d2h_GBps": round(d, 1)}), flush=True)
