@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 
 #include "k1_2d.cuh"  // fma_rn, cp_async helpers
@@ -148,16 +149,20 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
       }
   };
 
-  auto body = [&](auto phase_tag, int it) SO2DR_INLINE {
+  // FAST = steady state of a CTA whose whole tile is interior: every stage
+  // consumes and emits interior planes, no ring pass-through, no grid-edge
+  // masking -- all range checks compile away (as in the 2D K1).
+  auto body = [&](auto phase_tag, auto fast_tag, int it) SO2DR_INLINE {
     constexpr int PH = decltype(phase_tag)::value;
+    constexpr bool FAST = decltype(fast_tag)::value;
     const int par = it & 1, ppar = par ^ 1;
     const int row0 = lo0 + it;
 #pragma unroll
     for (int u = S; u >= 1; --u) {
       const int A = row0 - u - (u - 1) * R;
       const int Ez = A - R;
-      const bool consume = A >= lo[u - 1] && A < hi[u - 1];
-      const bool emit = Ez >= lo[u] && Ez < hi[u];
+      const bool consume = FAST || (A >= lo[u - 1] && A < hi[u - 1]);
+      const bool emit = FAST || (Ez >= lo[u] && Ez < hi[u]);
 
       // neighbourhood of the consumed plane: rows yt-R .. yt+VY-1+R,
       // cols xt-R .. xt+V-1+R
@@ -218,13 +223,14 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
       if (emit) {
         constexpr int se = (PH - 2 * R + 2 * E) % E;
         T outv[VY][V];
-        const bool ring_plane = Ez < a.iz0 || Ez >= a.iz1;
+        const bool ring_plane = !FAST && (Ez < a.iz0 || Ez >= a.iz1);
 #pragma unroll
         for (int j = 0; j < VY; ++j)
 #pragma unroll
           for (int k = 0; k < V; ++k) {
             outv[j][k] = acc[u - 1][se][j][k];
-            if (ring_plane || (ringmask & (1u << (j * V + k)))) outv[j][k] = passthru(Ez, j, k);
+            if constexpr (!FAST)
+              if (ring_plane || (ringmask & (1u << (j * V + k)))) outv[j][k] = passthru(Ez, j, k);
           }
         if (u == S) {
           T* dst = a.out + (int64_t)(Ez - sz0) * a.plane_stride;
@@ -246,23 +252,54 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
     // stage 0
     issue(row0 + RING - 1);
     cp_async_wait<RING - 1>();
-    if (row0 < hi0) {
+    if (FAST || row0 < hi0) {
 #pragma unroll
       for (int j = 0; j < VY; ++j)
 #pragma unroll
         for (int k = 0; k < V; ++k)
-          cur[0][j][k] = (inmask & (1u << (j * V + k))) ? ring[row0 & (RING - 1)][j][tid * V + k] : T(0);
+          cur[0][j][k] = (FAST || (inmask & (1u << (j * V + k)))) ? ring[row0 & (RING - 1)][j][tid * V + k] : T(0);
       publish_edges(par, 0, cur[0]);
     }
     __syncthreads();
   };
 
-  int it = 0;
-  while (it < n_iter) {
-    [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
-      ((it < n_iter ? (body(std::integral_constant<int, Ps>{}, it), ++it, void()) : void()), ...);
-    }(std::make_integer_sequence<int, E>{});
+  // steady-state window [f_lo, f_hi) of iterations (same derivation as 2D);
+  // CTA-uniform, so the one barrier per iteration stays uniform
+  int f_lo = 0, f_hi = hi0 - lo0;
+#pragma unroll
+  for (int u = 1; u <= S; ++u) {
+    const int c = lo0 - u - (u - 1) * R;
+    f_lo = max(f_lo, lo[u - 1] - c);
+    f_hi = min(f_hi, hi[u - 1] - c);
+    f_lo = max(f_lo, max(lo[u], a.iz0) + R - c);
+    f_hi = min(f_hi, min(hi[u], a.iz1) + R - c);
   }
+  const bool tile_interior = cx0 >= a.i0 && cx0 + 32 * V <= a.i1 && cy0 >= a.i0 && cy0 + NW * VY <= a.i1;
+  if (!tile_interior) f_hi = f_lo;
+
+  int it = 0;
+  auto run_general = [&](int stop) SO2DR_INLINE {
+    while (it < stop) {
+      [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
+        ((it < stop ? (body(std::integral_constant<int, Ps>{}, std::false_type{}, it), ++it, void()) : void()),
+         ...);
+      }(std::make_integer_sequence<int, E>{});
+    }
+  };
+  // (the radius-2 box's 125-tap pipeline has no register room for a second
+  // copy of the loop: it runs the general path only, no spill)
+  if constexpr (!(KIND == KBOX && R >= 2)) {
+    const int fl = (f_lo + E - 1) / E * E;
+    if (f_hi - fl >= E) {
+      run_general(fl);
+      while (it + E <= f_hi) {
+        [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
+          ((body(std::integral_constant<int, Ps>{}, std::true_type{}, it), ++it), ...);
+        }(std::make_integer_sequence<int, E>{});
+      }
+    }
+  }
+  run_general(n_iter);
   cp_async_wait<0>();
 }
 
@@ -270,11 +307,23 @@ namespace {
 
 inline int fdiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
-template <typename T, int R, int S, int KIND>
+// Tile shape of the 3D K1 per thread (V x VY cells) and CTA size. Default
+// 2x2 cells, 512 threads. SO2DR_K1_3D=42 / 44 select 4x2 / 4x4 cells on 256
+// threads for fp32 radius 1 (experiments: more FMAs per shuffle/LDS/barrier).
+inline int k1_3d_shape() {
+  static int v = [] {
+    const char* e = std::getenv("SO2DR_K1_3D");
+    return e ? std::atoi(e) : 22;
+  }();
+  return v;
+}
+
+template <typename T, int R, int S, int KIND, int V = 2, int VY = 2,
+          int NT = (sizeof(T) == 8 && R == 2) ? 256 : 512>
 cudaError_t launch3(const K1Launch& L, cudaStream_t stream) {
   // 512 threads cap registers at 128; the fp64 radius-2 box needs more (a spill
   // otherwise), so it runs 256-thread CTAs
-  constexpr int NT = (sizeof(T) == 8 && R == 2) ? 256 : 512, NW = NT / 32, V = 2, VY = 2, H = R * S;
+  constexpr int NW = NT / 32, H = R * S;
   constexpr size_t smem = sizeof(T) * (4 * VY * NT * V + 2 * S * (NW + 2) * 2 * R * 32 * V);
   static_assert(smem <= 227 * 1024, "3D K1 shared memory");
   auto kern = k1_stencil3d<T, R, S, KIND, V, VY, NT>;
@@ -336,7 +385,15 @@ cudaError_t launch3_s(const K1Launch& L, cudaStream_t stream) {
   if constexpr (S > maxs3d<T>(R)) {
     return cudaErrorInvalidValue;
   } else {
-    if (L.steps == S) return launch3<T, R, S, KIND>(L, stream);
+    if (L.steps == S) {
+      if constexpr (sizeof(T) == 4 && R == 1) {
+        if (k1_3d_shape() == 42) return launch3<T, R, S, KIND, 4, 2, 256>(L, stream);
+        if constexpr (S <= 2) {
+          if (k1_3d_shape() == 44) return launch3<T, R, S, KIND, 4, 4, 256>(L, stream);
+        }
+      }
+      return launch3<T, R, S, KIND>(L, stream);
+    }
     return launch3_s<T, R, KIND, S + 1>(L, stream);
   }
 }

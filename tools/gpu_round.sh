@@ -121,6 +121,15 @@ for s in $steps; do
       echo "robust2 rc=$?" >> $OUT/summary.txt; cat $OUT/pipe_sweep_robust2.log >> $OUT/summary.txt
       timeout 300 python tools/pipe_profile.py 92160 64 4 3 > $OUT/pp_d64.log 2>&1
       head -1 $OUT/pp_d64.log >> $OUT/summary.txt; grep -E "c(20|21|22) (htod|dtoh)" $OUT/pp_d64.log >> $OUT/summary.txt ;;
+    k3d)
+      for sh in ${SHAPES:-22 42 44}; do
+        SO2DR_K1_3D=$sh SZ3=768 STENCILS=star3d1r,box3d1r KS=1,2,4 timeout 900 python tools/k1_bench.py > $OUT/k3d_$sh.log 2>&1
+        echo "shape=$sh" >> $OUT/summary.txt; cat $OUT/k3d_$sh.log >> $OUT/summary.txt
+      done
+      timeout 900 python -m pytest tests/test_gpu_3d_f64.py tests/test_gpu_fullsize.py -x -q > $OUT/pytest_3d.log 2>&1; echo "pytest 3d rc=$?" >> $OUT/summary.txt ;;
+    ncu3d)
+      timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_stencil3d -s 1 -c 1 -o $OUT/k1_3d_star_k4 -f \
+        python tools/k1_one3d.py 4 768 star > $OUT/k1_3d.log 2>&1; echo "ncu3d rc=$?" >> $OUT/summary.txt ;;
     ncu)
       # launch list of one bench step (e2e leg): every launch with its device time
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
