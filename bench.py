@@ -201,6 +201,9 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # torchrun exports OMP_NUM_THREADS=1 to every rank; the reference CPU solver on
+    # rank 0 gets all host cores (set before libgomp is loaded with oracle/_ref)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     samples = []
     for i in range(args.warmup + args.steps):
         cb = cpu_baseline_sample()

@@ -130,6 +130,13 @@ for s in $steps; do
     ncu3d)
       timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_stencil3d -s 1 -c 1 -o $OUT/k1_3d_star_k4 -f \
         python tools/k1_one3d.py 4 768 star > $OUT/k1_3d.log 2>&1; echo "ncu3d rc=$?" >> $OUT/summary.txt ;;
+    multi)
+      SO2DR_SHARE_DEVICE=1 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 1 --no-value-leg > $OUT/bench_n2_shared.log 2>&1
+      echo "multi rc=$?" >> $OUT/summary.txt; tail -1 $OUT/bench_n2_shared.log | cut -c1-1500 >> $OUT/summary.txt
+      timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 \
+        bench.py --impl reference --gpus 2 --steps 1 --warmup 0 > $OUT/bench_ref_n2.log 2>&1
+      echo "ref n2 rc=$?" >> $OUT/summary.txt; tail -1 $OUT/bench_ref_n2.log | cut -c1-300 >> $OUT/summary.txt ;;
     ncu)
       # launch list of one bench step (e2e leg): every launch with its device time
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
