@@ -207,6 +207,12 @@ cudaError_t launch_2d_s(const K1Launch& L, cudaStream_t stream) {
     if (L.steps == S) {
       if constexpr (sizeof(T) == 4 && R == 1 && KIND != KGRAD) {
         if (k1_v_override() == 2) return launch_2d_fixed<T, R, S, KIND, 2, 2>(L, stream);
+        // 8 cells per lane (scalar FFMA; 198 registers at S = 4, 1 CTA/SM): 77% of
+        // the steady-state loop's instructions are FFMA vs 68% at V = 4
+        if constexpr (S <= 4) {
+          if (k1_v_override() == 8 && k1_impl_override() != 1)
+            return launch_2d_fixed<T, R, S, KIND, 8, 1, false>(L, stream);
+        }
         // Paired-strip kernel (SO2DR_K1_IMPL=p2; S = 3..4 only: at S > 4 it needs
         // V = 2 and spills). In-core it is within noise of pk (+-3% at S = 4,
         // profiles/r01_k1); inside the bench pipeline (d=64, ~1500-row

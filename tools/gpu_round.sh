@@ -137,6 +137,14 @@ for s in $steps; do
       timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 \
         bench.py --impl reference --gpus 2 --steps 1 --warmup 0 > $OUT/bench_ref_n2.log 2>&1
       echo "ref n2 rc=$?" >> $OUT/summary.txt; tail -1 $OUT/bench_ref_n2.log | cut -c1-300 >> $OUT/summary.txt ;;
+    v8)
+      for v in 4 8; do
+        SO2DR_K1_V=$v SZ=32768 STENCILS=box2d1r,star2d1r KS=2,4 timeout 600 python tools/k1_bench.py > $OUT/k1_v$v.log 2>&1
+        echo "V=$v" >> $OUT/summary.txt; cat $OUT/k1_v$v.log >> $OUT/summary.txt
+        SO2DR_K1_V=$v timeout 900 python bench.py --steps 3 --warmup 2 --no-cpu-baseline > $OUT/bench_v$v.log 2>&1
+        tail -1 $OUT/bench_v$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench V', $v, 'value', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), 'K1 ms', round(d['roofline']['avg_launch_ms'],4), 'frac', round(d['roofline']['frac'],3))" >> $OUT/summary.txt
+      done
+      SO2DR_K1_V=8 timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py -x -q > $OUT/pytest_v8.log 2>&1; echo "pytest v8 rc=$?" >> $OUT/summary.txt ;;
     ncu)
       # launch list of one bench step (e2e leg): every launch with its device time
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
