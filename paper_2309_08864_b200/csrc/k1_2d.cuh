@@ -34,6 +34,14 @@
 //    (no local-memory indexing), and the steady state (every stage consumes
 //    and emits an interior row, no ring column in the strip) runs a variant
 //    with all range checks compiled away.
+//
+// Three arithmetic variants share this pipeline (k1_2d_impl.cuh picks one):
+//  * k1_stencil2d<..., SCALAR=true>: one scalar FFMA per tap -- the fp32 default
+//    (FFMA reaches the FMA peak on sm_100 as well as FFMA2, and without register
+//    pairs ptxas needs no operand moves: profiles/r01_k1/scalar_vs_pk.txt);
+//  * k1_stencil2d_pk: packed FFMA2 on cell pairs (k, k+V/2) (SO2DR_K1_IMPL=pk);
+//  * k1_stencil2d<double>: DFMA (fp64), and the gradient's pinned expression.
+// The paired-strip FFMA2 kernel lives in k1_2d_p2.cuh (SO2DR_K1_IMPL=p2).
 #pragma once
 
 #include <cuda_runtime.h>
