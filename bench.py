@@ -411,6 +411,10 @@ def main():
         "binding_roofline": {"R_pcie": r_pcie, "R_hbm": r_hbm, "R_bind": r_bind, "unit": UNIT,
                              "frac_e2e": e2e_v / r_bind, "frac_value_vs_R_hbm": (val_v / r_hbm) if val_v else None,
                              "pcie_measured": pc,
+                             "pcie_achieved_GBps_per_dir": {
+                                 "h2d": e2e_res["h2d"] / (e2e_res["device_ms_total"] / 1e3) / 1e9,
+                                 "d2h": e2e_res["d2h"] / (e2e_res["device_ms_total"] / 1e3) / 1e9,
+                                 "note": "ledger bytes / e2e device time (includes pipeline fill and drain)"},
                              "formula": "R_pcie = G*BW_pcie_dir(duplex)*S_TB/b ; R_hbm = G*BW_hbm/(2b/k_on + 2b/S_TB)"},
         "cpu_baseline": cb,
         "clocks": clocks,
