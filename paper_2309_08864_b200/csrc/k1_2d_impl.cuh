@@ -51,15 +51,18 @@ inline int k1_impl_override() {
   return v;
 }
 
-// Work items per resident warp (row segments x strips). Default 8; shorter
-// segments balance the tail, longer ones amortise the R*S warm-up rows.
-// SO2DR_K1_IPW=n overrides (experiments).
-inline int k1_items_per_warp() {
+// Work items per resident warp (row segments x strips): more items balance
+// the tail, longer segments amortise the R*S warm-up rows and the S-stage
+// pipeline fill. Measured (profiles/r01_k1/ipw_*): launches over a whole grid
+// (32768 rows) are best at 8 (6: -6%), the ~1500-row launches of the bench's
+// d=64 chunks at 6 (8: -3%). SO2DR_K1_IPW=n overrides (experiments).
+inline int k1_items_per_warp(int height) {
   static int v = [] {
     const char* s = std::getenv("SO2DR_K1_IPW");
-    return s ? std::max(1, std::atoi(s)) : 8;
+    return s ? std::max(1, std::atoi(s)) : 0;
   }();
-  return v;
+  if (v) return v;
+  return height < 4096 ? 6 : 8;
 }
 
 template <typename T, int R, int S, int KIND, int V, int MINB,
@@ -125,7 +128,7 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   const int resident_warps = sms * occ * NW;
   const int min_seg = std::max(48, 6 * (H + S * (R + 1)));
   const int max_ns = std::max(1, height / min_seg);
-  int ns = std::max(1, (k1_items_per_warp() * resident_warps + a.warps_x - 1) / a.warps_x);
+  int ns = std::max(1, (k1_items_per_warp(height) * resident_warps + a.warps_x - 1) / a.warps_x);
   ns = std::min(ns, max_ns);
   a.seg = (height + ns - 1) / ns;
   a.nseg = (height + a.seg - 1) / a.seg;
@@ -187,7 +190,7 @@ cudaError_t launch_2d_p2(const K1Launch& L, cudaStream_t stream) {
   const int resident_warps = sms * occ * NW;
   const int min_seg = std::max(48, 6 * (H + S * (R + 1)));
   const int max_ns = std::max(1, height / min_seg);
-  int ns = std::max(1, (k1_items_per_warp() * resident_warps + np - 1) / np);
+  int ns = std::max(1, (k1_items_per_warp(height) * resident_warps + np - 1) / np);
   ns = std::min(ns, max_ns);
   a.seg = (height + ns - 1) / ns;
   a.nseg = (height + a.seg - 1) / a.seg;

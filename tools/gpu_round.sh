@@ -78,7 +78,7 @@ for s in $steps; do
       timeout 900 python tools/pcie_pipe3.py > $OUT/pcie_pipe3.log 2>&1; echo "pcpipe3 rc=$?" >> $OUT/summary.txt
       cat $OUT/pcie_pipe3.log >> $OUT/summary.txt ;;
     ipw)
-      for ipw in 4 8 16 32; do for impl in pk p2; do
+      for ipw in ${IPWS:-4 8 16 32}; do for impl in ${IMPLS:-pk p2}; do
         SO2DR_K1_IPW=$ipw SO2DR_K1_IMPL=$impl SZ=32768 STENCILS=box2d1r KS=2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_ipw${ipw}_${impl}.log 2>&1
         echo "ipw=$ipw impl=$impl" >> $OUT/summary.txt; cat $OUT/k1_ipw${ipw}_${impl}.log >> $OUT/summary.txt
       done; done ;;
