@@ -490,7 +490,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
 // moves (each FMA-pipe instruction costs 2 issue cycles per SMSP; FFMA2 does
 // 64 fmas in them, a scalar FFMA 32). Each half is an IEEE round-to-nearest
 // fma: results are bit-identical to the scalar chain.
-template <int R, int S, int KIND, int V, int NT>
+template <int R, int S, int KIND, int V, int NT, bool HYB = false>
 __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int sg,
                                            float (&ring)[K1Plan2D<float, R, S, KIND, V, NT>::RING][NT * V]) {
   using T = float;
@@ -619,7 +619,17 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
       };
       uint64_t op[NP];  // op[j] = (s_j, s_{j+HV})
 #pragma unroll
-      for (int j = 0; j < NP; ++j) op[j] = (j >= R && j < R + HV) ? in[j - R] : pack2(sval(j), sval(j + HV));
+      for (int j = 0; j < NP; ++j)
+        op[j] = (HYB || (j >= R && j < R + HV)) ? (j >= R && j < R + HV ? in[j - R] : 0ull)
+                                                : pack2(sval(j), sval(j + HV));
+      // one tap: FFMA2 on an in-register pair, or (HYB) two scalar FFMAs on
+      // the halves when the operand pair would need a shuffled halo value
+      auto tap = [&](float w, int j, uint64_t x) SO2DR_INLINE -> uint64_t {
+        if (!HYB || (j >= R && j < R + HV)) return fma2p(w, op[j], x);
+        float xl, xh;
+        unpack2(x, xl, xh);
+        return pack2(__fmaf_rn(w, sval(j), xl), __fmaf_rn(w, sval(j + HV), xh));
+      };
 
       if (consume) {
 #pragma unroll
@@ -631,12 +641,12 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
             uint64_t x = (m == 0) ? 0ull : ap[u - 1][sl][k];
             if constexpr (KIND == KBOX) {
 #pragma unroll
-              for (int dx = -R; dx <= R; ++dx) x = fma2p(a.w[(dy + R) * E + dx + R], op[R + k + dx], x);
+              for (int dx = -R; dx <= R; ++dx) x = tap(a.w[(dy + R) * E + dx + R], R + k + dx, x);
             } else if (dy != 0) {
-              x = fma2p(a.w[(dy + R) * E + R], op[R + k], x);
+              x = tap(a.w[(dy + R) * E + R], R + k, x);
             } else {
 #pragma unroll
-              for (int dx = -R; dx <= R; ++dx) x = fma2p(a.w[R * E + dx + R], op[R + k + dx], x);
+              for (int dx = -R; dx <= R; ++dx) x = tap(a.w[R * E + dx + R], R + k + dx, x);
             }
             ap[u - 1][sl][k] = x;
           }
@@ -753,7 +763,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
   }
 }
 
-template <int R, int S, int KIND, int V, int NT, int MINB>
+template <int R, int S, int KIND, int V, int NT, int MINB, bool HYB = false>
 __global__ void __launch_bounds__(NT, MINB) k1_stencil2d_pk(const K1Args2D<float> a) {
   __shared__ __align__(16) float ring[K1Plan2D<float, R, S, KIND, V, NT>::RING][NT * V];
   const int lane = threadIdx.x & 31;
@@ -765,7 +775,7 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d_pk(const K1Args2D<float
     if (item >= total) break;
     int wx, sg;
     k1_item_coords(a, item, wx, sg);
-    k1_item_pk<R, S, KIND, V, NT>(a, wx, sg, ring);
+    k1_item_pk<R, S, KIND, V, NT, HYB>(a, wx, sg, ring);
   }
 }
 

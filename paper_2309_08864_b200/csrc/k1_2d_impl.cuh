@@ -46,7 +46,7 @@ inline int k1_impl_override() {
   static int v = [] {
     const char* s = std::getenv("SO2DR_K1_IMPL");
     if (!s) return 0;
-    return std::strcmp(s, "p2") == 0 ? 2 : std::strcmp(s, "pk") == 0 ? 1 : 0;
+    return std::strcmp(s, "p2") == 0 ? 2 : std::strcmp(s, "pk") == 0 ? 1 : std::strcmp(s, "hyb") == 0 ? 4 : 0;
   }();
   return v;
 }
@@ -66,7 +66,7 @@ inline int k1_items_per_warp(int height) {
 }
 
 template <typename T, int R, int S, int KIND, int V, int MINB,
-          bool PACK = std::is_same_v<T, float> && KIND != KGRAD && V % 2 == 0>
+          bool PACK = std::is_same_v<T, float> && KIND != KGRAD && V % 2 == 0, bool HYB = false>
 cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   constexpr int NT = kThreads2D;
   constexpr int H = R * S;
@@ -115,7 +115,7 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   constexpr bool packed = PACK;
   auto kern = [] {
     if constexpr (packed)
-      return k1_stencil2d_pk<R, S, KIND, V, NT, MINB>;
+      return k1_stencil2d_pk<R, S, KIND, V, NT, MINB, HYB>;
     else
       return k1_stencil2d<T, R, S, KIND, V, NT, MINB, std::is_same_v<T, float> && KIND != KGRAD>;
   }();
@@ -238,6 +238,9 @@ cudaError_t launch_2d_s(const K1Launch& L, cudaStream_t stream) {
         return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1, false>(L, stream);
       } else {
         if constexpr (sizeof(T) == 4 && KIND != KGRAD) {
+          // hybrid: FFMA2 where the operand pair is in registers, scalar FFMA
+          // for the halo taps (SO2DR_K1_IMPL=hyb, experiment)
+          if (k1_impl_override() == 4) return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1, true, true>(L, stream);
           if (k1_impl_override() != 1) return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1, false>(L, stream);
         }
         return launch_2d_fixed<T, R, S, KIND, v2d<T>(R), 1>(L, stream);

@@ -145,6 +145,14 @@ for s in $steps; do
         tail -1 $OUT/bench_v$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench V', $v, 'value', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), 'K1 ms', round(d['roofline']['avg_launch_ms'],4), 'frac', round(d['roofline']['frac'],3))" >> $OUT/summary.txt
       done
       SO2DR_K1_V=8 timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py -x -q > $OUT/pytest_v8.log 2>&1; echo "pytest v8 rc=$?" >> $OUT/summary.txt ;;
+    hyb)
+      for impl in default hyb; do
+        SO2DR_K1_IMPL=$impl SZ=32768 STENCILS=box2d1r,star2d1r,box2d2r KS=2,4,8 timeout 900 python tools/k1_bench.py > $OUT/k1_$impl.log 2>&1
+        echo "impl=$impl" >> $OUT/summary.txt; cat $OUT/k1_$impl.log >> $OUT/summary.txt
+        SO2DR_K1_IMPL=$impl timeout 900 python bench.py --steps 3 --warmup 2 --no-cpu-baseline > $OUT/bench_$impl.log 2>&1
+        tail -1 $OUT/bench_$impl.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', '$impl', 'value', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), 'K1 ms', round(d['roofline']['avg_launch_ms'],4), 'frac', round(d['roofline']['frac'],3))" >> $OUT/summary.txt
+      done
+      SO2DR_K1_IMPL=hyb timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py -x -q > $OUT/pytest_hyb.log 2>&1; echo "pytest hyb rc=$?" >> $OUT/summary.txt ;;
     ncu)
       # launch list of one bench step (e2e leg): every launch with its device time
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
