@@ -1,5 +1,6 @@
 """Every fp32 K1 variant must stay bit-exact with the oracle: the default
-scalar-FFMA pipeline, the packed FFMA2 kernel (SO2DR_K1_IMPL=pk) and the
+scalar-FFMA pipeline, the packed FFMA2 kernel (SO2DR_K1_IMPL=pk), the hybrid
+FFMA2/FFMA kernel (SO2DR_K1_IMPL=hyb) and the
 paired-strip kernel (SO2DR_K1_IMPL=p2, S = 3..4). Run in a subprocess: the
 variant is chosen once per process."""
 import os
@@ -33,7 +34,7 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("impl", ["p2", "pk", "default"])
+@pytest.mark.parametrize("impl", ["p2", "pk", "hyb", "default"])
 def test_k1_variant_bit_exact(impl):
     env = dict(os.environ)
     env.pop("SO2DR_K1_IMPL", None)
