@@ -280,10 +280,14 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
       if (ok) issue_vec<T, VEC>(dst + v, src + v, cpb, xt + v, a.pitch);
     cp_async_commit();
   };
+  // steady-state addressing off a running row offset (no 64-bit multiplies
+  // per row): off = (row0 - sy0) * pitch, advanced by one row per iteration;
+  // load row = row0 + kRing - 1, store row = row0 - S(R+1)
+  int64_t off = (int64_t)(lo0 - sy0) * a.pitch;
+  const T* ld_lane = src_col + (int64_t)(kRing - 1) * a.pitch;
+  T* st_lane = a.out + xt - (int64_t)(S * (R + 1)) * a.pitch;
   auto issue_fast = [&](int row) SO2DR_INLINE {
-    if (row < hi0)
-      issue_inrow<V * (int)sizeof(T)>(my_ring + (row & (kRing - 1)) * (NT * V),
-                                      src_col + (int64_t)(row - sy0) * a.pitch);
+    if (row < hi0) issue_inrow<V * (int)sizeof(T)>(my_ring + (row & (kRing - 1)) * (NT * V), ld_lane + off);
     cp_async_commit();
   };
 #pragma unroll
@@ -420,7 +424,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
           }
         }
         if (u == S) {
-          T* dst = gout + (int64_t)(Erow - sy0) * a.pitch + xt;
+          T* dst = FAST ? st_lane + off : gout + (int64_t)(Erow - sy0) * a.pitch + xt;
 #pragma unroll
           for (int k = 0; k < V; ++k)
             if (smask & (1u << k)) dst[k] = outv[k];
@@ -442,6 +446,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
 #pragma unroll
       for (int k = 0; k < V; ++k) cur[0][k] = src[k];
     }
+    off += a.pitch;
   };
 
   // ---- steady-state window [f_lo, f_hi): every stage consumes a stored row
