@@ -576,11 +576,13 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
       if (ok) issue_vec<T, VEC>(dst + v, src + v, cpb, xt + v, a.pitch);
     cp_async_commit();
   };
-  // steady state: the strip owns no column outside the interior
+  // steady state: the strip owns no column outside the interior; addressing
+  // off a running row offset (off = (row0 - sy0) * pitch, see k1_item)
+  int64_t off = (int64_t)(lo0 - sy0) * a.pitch;
+  const T* ld_lane = src_col + (int64_t)(kRing - 1) * a.pitch;
+  T* st_lane = a.out + xt - (int64_t)(S * (R + 1)) * a.pitch;
   auto issue_fast = [&](int row) SO2DR_INLINE {
-    if (row < hi0)
-      issue_inrow<V * (int)sizeof(T)>(my_ring + (row & (kRing - 1)) * (NT * V),
-                                      src_col + (int64_t)(row - sy0) * a.pitch);
+    if (row < hi0) issue_inrow<V * (int)sizeof(T)>(my_ring + (row & (kRing - 1)) * (NT * V), ld_lane + off);
     cp_async_commit();
   };
 #pragma unroll
@@ -676,7 +678,7 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
           }
         }
         if (u == S) {
-          T* dst = a.out + (int64_t)(Erow - sy0) * a.pitch + xt;
+          T* dst = FAST ? st_lane + off : a.out + (int64_t)(Erow - sy0) * a.pitch + xt;
 #pragma unroll
           for (int k = 0; k < V; ++k)
             if (smask & (1u << k)) dst[k] = cell(outp, k);
@@ -693,6 +695,7 @@ __device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int
 #pragma unroll
       for (int k = 0; k < HV; ++k) cp0[k] = pack2(src[k], src[k + HV]);
     }
+    off += a.pitch;
   };
 
   int f_lo = 0, f_hi = hi0 - lo0;
