@@ -133,6 +133,21 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
   for (int d = 0; d < RING - 1; ++d) issue(lo0 + d);
   __syncthreads();
 
+  // steady-state addressing off a running plane offset (poff = (row0 - sz0) *
+  // plane_stride, advanced once per iteration): load plane row0 + RING - 1,
+  // store plane row0 - S(R+1); the thread's (y, x) part is loop-invariant
+  int64_t poff = (int64_t)(lo0 - sz0) * a.plane_stride;
+  const T* ld_thr = a.in + (int64_t)(RING - 1) * a.plane_stride + (int64_t)yt * a.pitch + xt;
+  T* st_thr = a.out - (int64_t)(S * (R + 1)) * a.plane_stride + (int64_t)yt * a.pitch + xt;
+  auto issue_fast = [&](int plane) SO2DR_INLINE {
+    if (plane < hi0) {
+#pragma unroll
+      for (int j = 0; j < VY; ++j)
+        issue_inrow<V * (int)sizeof(T)>(&ring[plane & (RING - 1)][j][tid * V], ld_thr + poff + (int64_t)j * a.pitch);
+    }
+    cp_async_commit();
+  };
+
   auto passthru = [&](int plane, int j, int k) SO2DR_INLINE -> T {
     const int x = xt + k, y = yt + j;
     if (x < 0 || x >= a.p || y < 0 || y >= a.p) return T(0);
@@ -233,12 +248,21 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
               if (ring_plane || (ringmask & (1u << (j * V + k)))) outv[j][k] = passthru(Ez, j, k);
           }
         if (u == S) {
-          T* dst = a.out + (int64_t)(Ez - sz0) * a.plane_stride;
+          if constexpr (FAST) {
+            T* dst = st_thr + poff;
 #pragma unroll
-          for (int j = 0; j < VY; ++j)
+            for (int j = 0; j < VY; ++j)
 #pragma unroll
-            for (int k = 0; k < V; ++k)
-              if (smask & (1u << (j * V + k))) dst[(int64_t)(yt + j) * a.pitch + xt + k] = outv[j][k];
+              for (int k = 0; k < V; ++k)
+                if (smask & (1u << (j * V + k))) dst[(int64_t)j * a.pitch + k] = outv[j][k];
+          } else {
+            T* dst = a.out + (int64_t)(Ez - sz0) * a.plane_stride;
+#pragma unroll
+            for (int j = 0; j < VY; ++j)
+#pragma unroll
+              for (int k = 0; k < V; ++k)
+                if (smask & (1u << (j * V + k))) dst[(int64_t)(yt + j) * a.pitch + xt + k] = outv[j][k];
+          }
         } else {
 #pragma unroll
           for (int j = 0; j < VY; ++j)
@@ -250,7 +274,10 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
     }
 
     // stage 0
-    issue(row0 + RING - 1);
+    if constexpr (FAST)
+      issue_fast(row0 + RING - 1);
+    else
+      issue(row0 + RING - 1);
     cp_async_wait<RING - 1>();
     if (FAST || row0 < hi0) {
 #pragma unroll
@@ -260,6 +287,7 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
           cur[0][j][k] = (FAST || (inmask & (1u << (j * V + k)))) ? ring[row0 & (RING - 1)][j][tid * V + k] : T(0);
       publish_edges(par, 0, cur[0]);
     }
+    poff += a.plane_stride;
     __syncthreads();
   };
 
