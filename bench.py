@@ -7,9 +7,11 @@ budget on one B200, 64 timesteps: sz=92160 (92162^2 fp32 = 33.98 GB host grid),
 16 GiB real HBM budget, d=64 chunks, S_TB=64 (one round), k_on=4, N_strm=3.
 A "step" is one full so2dr run (64 timesteps over the whole grid).
 
-  value : same run with the grid already resident in HBM (copies become D2D)
-  e2e   : the headline -- C-ABI so2dr_run on the pinned HOST grid, all PCIe
-          traffic inside the timed region (CUDA events, first H2D -> last D2H)
+  value, e2e : the BASELINE metric -- C-ABI so2dr_run on the pinned HOST grid,
+          all PCIe traffic inside the timed region (CUDA events, first H2D ->
+          last D2H); `value` == `e2e.value`
+  hbm_resident : the same run with the grid already resident in HBM (the
+          transfers become D2D copies) -- explains the kernel side, not the metric
 
 Multi-GPU (torchrun): the d chunks are slab-partitioned over ranks (weak scaling:
 each rank streams a ~34 GB slab of a sz~92160*sqrt(N) grid); inter-slab halos
@@ -155,71 +157,147 @@ def pcie_probe(torch, dev):
     return out
 
 
-def cpu_baseline_sample():
-    """The reference's own CPU solver (oracle/_ref = /root/reference sources, -O3
-    -ffp-contract=off -fopenmp) on a bounded sample of the workload: same stencil,
-    d, S_TB, k_on, n; sz reduced 3x (1/9 of the cells, ~10 s on 16 host threads)."""
+def _ref_engine_sample(sz):
+    """One reference run_engine(so2dr) call (oracle/_ref: the unmodified reference
+    sources, -O3 -ffp-contract=off -fopenmp) on a box2d1r grid of side sz with the
+    bench's d, S_TB, k_on, n. Returns (GCell/s from RunReport.wall_seconds, s)."""
     import ctypes
 
     import pyoracle as o
 
-    sz, d = SZ1 // 3, D_PER_RANK
-    cells = (sz + 2 * R) ** 2
+    R_ = o.ref()
+    d = D_PER_RANK
+    g = np.empty((sz + 2 * R, sz + 2 * R), np.float32)
+    R_.ref_init_grid(sz, R, 42, g.ctypes.data)
+    out = np.empty_like(g)
+    led = (ctypes.c_uint64 * 9)()
+    peak, wall = ctypes.c_uint64(), ctypes.c_double()
+    err = ctypes.create_string_buffer(256)
+    t0 = time.perf_counter()
+    rc = R_.ref_run_engine(0, 0, R, None, (ctypes.c_int * 8)(sz, R, d, S_TB, K_ON, NSTRM, NSTEPS, 2),
+                           (ctypes.c_int * 2)(K_ON, 32), 64 << 20, 1 << 40, 760e9, 15.75e9, 0, 0,
+                           g.ctypes.data, out.ctypes.data, led, ctypes.byref(peak), ctypes.byref(wall), err, 256)
+    t = time.perf_counter() - t0
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    sec = wall.value if wall.value > 0 else t
+    return sz * sz * NSTEPS / sec / 1e9, sec
+
+
+def _ref_serial_sample():
+    """The reference's serial oracle run_reference (stencil.cpp:162-174, one core):
+    box2d1r sz=8192, 16 steps (1.07 G updates)."""
+    import ctypes
+
+    import pyoracle as o
+
+    R_ = o.ref()
+    sz, n = 8192, 16
+    g = np.empty((sz + 2 * R, sz + 2 * R), np.float32)
+    R_.ref_init_grid(sz, R, 42, g.ctypes.data)
+    out = np.empty_like(g)
+    err = ctypes.create_string_buffer(256)
+    t0 = time.perf_counter()
+    rc = R_.ref_run_reference(0, R, None, sz, R, g.ctypes.data, n, out.ctypes.data, err, 256)
+    sec = time.perf_counter() - t0
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    return {"value": sz * sz * n / sec / 1e9, "unit": UNIT, "cores": 1,
+            "sample": f"reference run_reference (serial ping-pong oracle) box2d1r sz={sz} n={n} in {sec:.2f} s"}
+
+
+def _ref_desc():
+    import pyoracle as o
+
+    bi = o.ref_build_info()
+    s = f"-O3 -march={bi['march']} -ffp-contract=off -fopenmp"
+    if bi.get("missing_isa"):
+        s += f" (the -march={bi.get('native_march')} build needs {','.join(bi['missing_isa'][:4])}... absent here)"
+    return s
+
+
+def cpu_baseline_sample():
+    """The reference's own CPU solver on a bounded sample of the workload: same
+    stencil, d, S_TB, k_on, n; sz reduced 3x (1/9 of the cells, ~10 s on 16
+    host threads)."""
+    import pyoracle as o
+
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     if o.have_ref():
-        R_ = o.ref()
-        g = np.empty((sz + 2 * R, sz + 2 * R), np.float32)
-        R_.ref_init_grid(sz, R, 42, g.ctypes.data)
-        out = np.empty_like(g)
-        led = (ctypes.c_uint64 * 9)()
-        peak, wall = ctypes.c_uint64(), ctypes.c_double()
-        err = ctypes.create_string_buffer(256)
-        t0 = time.perf_counter()
-        rc = R_.ref_run_engine(0, 0, R, None, (ctypes.c_int * 8)(sz, R, d, S_TB, K_ON, NSTRM, NSTEPS, 2),
-                               (ctypes.c_int * 2)(K_ON, 32), 64 << 20, 1 << 40, 760e9, 15.75e9, 0, 0,
-                               g.ctypes.data, out.ctypes.data, led, ctypes.byref(peak), ctypes.byref(wall), err, 256)
-        t = time.perf_counter() - t0
-        if rc != 0:
-            raise RuntimeError(err.value.decode())
-        sec = wall.value if wall.value > 0 else t
-        return {"value": sz * sz * NSTEPS / sec / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
-                "sample": f"reference run_engine(so2dr) box2d1r sz={sz} d={d} S_TB={S_TB} k_on={K_ON} n={NSTEPS} "
-                          f"({cells * 4 / 1e9:.2f} GB grid, {sz * sz * NSTEPS / 1e9:.1f} G updates) in {sec:.2f} s; "
-                          f"RunReport.wall_seconds, OMP_NUM_THREADS={cores}, 3 std::thread workers",
+        sz = SZ1 // 3
+        v, sec = _ref_engine_sample(sz)
+        return {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"reference run_engine(so2dr) box2d1r sz={sz} d={D_PER_RANK} S_TB={S_TB} k_on={K_ON} "
+                          f"n={NSTEPS} ({(sz + 2 * R) ** 2 * 4 / 1e9:.2f} GB grid, {sz * sz * NSTEPS / 1e9:.1f} G "
+                          f"updates) in {sec:.2f} s; RunReport.wall_seconds, OMP_NUM_THREADS={cores}, "
+                          f"3 std::thread workers; built {_ref_desc()}",
                 "seconds": sec}
     # fallback: the C restatement (serial)
-    g = o.init_grid(sz // 4, R, 42)
+    g = o.init_grid(SZ1 // 12, R, 42)
     t0 = time.perf_counter()
     o.run(g, o.BOX, R, o.box_weights(R), 4)
     sec = time.perf_counter() - t0
-    s4 = sz // 4
+    s4 = SZ1 // 12
     return {"value": s4 * s4 * 4 / sec / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"oracle port (serial C) box2d1r sz={s4} n=4 in {sec:.2f} s", "seconds": sec}
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU solver (run_engine(so2dr), all
+    host cores) on the bench's config. The full 34 GB grid would take ~5 min per
+    step, so each timed step is a bounded sample of the same workload: steps
+    alternate sz/3 (3.8 GB) and sz/2 (8.5 GB) grids with the same d, S_TB, k_on, n,
+    so the line shows GCell/s does not depend on the grid size (value = median
+    over all timed steps; per-size medians in cpu_baseline.by_size). Warm-up steps
+    run a sz/6 grid. The serial run_reference oracle is timed once beside it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     # torchrun exports OMP_NUM_THREADS=1 to every rank; the reference CPU solver on
     # rank 0 gets all host cores (set before libgomp is loaded with oracle/_ref)
     os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
-    samples = []
-    for i in range(args.warmup + args.steps):
+    import pyoracle as o
+
+    cores = int(os.environ["OMP_NUM_THREADS"])
+    if not o.have_ref():
         cb = cpu_baseline_sample()
-        if i >= args.warmup:
-            samples.append(cb)
-    v = statistics.median([s["value"] for s in samples])
-    cb = dict(samples[-1])
-    cb["value"] = v
-    cb.pop("seconds", None)
+        samples = [(0, cb["value"], cb["seconds"])]
+        by_size = {}
+        sample_desc = cb["sample"]
+        kind = "port"
+    else:
+        for _ in range(args.warmup):
+            _ref_engine_sample(SZ1 // 6)
+        samples = []
+        for i in range(args.steps):
+            sz = SZ1 // 3 if i % 2 == 0 else SZ1 // 2
+            v, sec = _ref_engine_sample(sz)
+            samples.append((sz, v, sec))
+        by_size = {}
+        for sz in sorted({s[0] for s in samples}):
+            vs = [s[1] for s in samples if s[0] == sz]
+            by_size[f"sz={sz}"] = {"GCell_s_median": statistics.median(vs), "samples": len(vs),
+                                   "grid_GB": (sz + 2 * R) ** 2 * 4 / 1e9}
+        sample_desc = (f"reference run_engine(so2dr) box2d1r, same d={D_PER_RANK} S_TB={S_TB} k_on={K_ON} "
+                       f"n={NSTEPS}; timed steps alternate sz={SZ1 // 3} and sz={SZ1 // 2} (the 34 GB sz={SZ1} "
+                       f"grid would take ~5 min per step); RunReport.wall_seconds, OMP_NUM_THREADS={cores}, "
+                       f"3 std::thread workers; built {_ref_desc()}")
+        kind = "reference"
+    v = statistics.median([s[1] for s in samples])
+    try:
+        serial = _ref_serial_sample() if o.have_ref() else None
+    except Exception as e:  # never fail the line on the serial column
+        serial = {"value": None, "sample": f"failed: {e}"}
+    cb = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample_desc, "by_size": by_size,
+          "serial_run_reference": serial}
     sz, d = geometry(1)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(s["seconds"] for s in samples),
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.median(s[2] for s in samples),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (splitmix64 init_grid, seed 42)",
-            "config": {"workload": workload_desc(1, sz, d) + "; reference CPU solver timed on a bounded sample "
-                       "(sz/3, same d/S_TB/k_on/n)"},
+            "config": {"workload": workload_desc(1, sz, d) + "; reference CPU solver timed on bounded samples "
+                       "(sz/3 and sz/2, same d/S_TB/k_on/n)"},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -233,7 +311,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--k-on", type=int, default=K_ON)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-value-leg", action="store_true")
+    ap.add_argument("--no-hbm-leg", "--no-value-leg", dest="no_hbm_leg", action="store_true")
     ap.add_argument("--pcie-probe-before", action="store_true",
                     help="measure the PCIe roof before the timed e2e leg (default: right after it; the torch "
                          "probe's pinned buffers cost the e2e leg ~1.5%% when taken before)")
@@ -320,7 +398,7 @@ def main():
 
     # ---- value leg: grid resident in HBM ---------------------------------
     value_res = None
-    if not args.no_value_leg:
+    if not args.no_hbm_leg:
         gdev = torch.empty(shape, dtype=torch.float32, device=dev)
         eng.init_rows(sz, R, 42, lo, hi, gdev)
         connect()
@@ -382,7 +460,7 @@ def main():
         except Exception as e:  # never fail the GPU line on the baseline
             cb = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference", "sample": f"failed: {e}"}
     line = {
-        "metric": METRIC, "value": val_v if val_v is not None else e2e_v, "unit": UNIT, "n_gpus": world,
+        "metric": METRIC, "value": e2e_v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": e2e_res["device_ms_total"] / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -391,9 +469,13 @@ def main():
                    "n": NSTEPS, "n_strm": NSTRM, "budget_bytes_per_gpu": BUDGET,
                    "grid_bytes": (sz + 2 * R) ** 2 * 4,
                    "l2": "no flush needed: every step streams the whole grid (>= 34 GB >> 126 MB L2)",
-                   "value_leg": "same so2dr run with the grid resident in HBM (transfers become D2D)",
+                   "value": "e2e: pinned host grid through the C ABI, H2D/D2H inside the timed region",
                    "timing": "CUDA events on the engine streams, first H2D enqueue -> last D2H completion, "
                              "summed over steps, max over ranks"},
+        "hbm_resident": ({"value": val_v, "unit": UNIT,
+                          "ms_per_step": value_res["device_ms_total"] / args.steps,
+                          "note": "same so2dr run with the grid resident in HBM (transfers become D2D); "
+                                  "not the BASELINE metric"} if value_res else None),
         "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": e2e_res["h2d"] // args.steps,
                 "d2h_bytes_per_step": e2e_res["d2h"] // args.steps,
                 "wall_s_per_step": e2e_res["wall_s"] / args.steps},
@@ -409,7 +491,7 @@ def main():
                              "note": "useful (non-redundant) FMAs: sz^2 * n * 9 per step; peak = measured FFMA2 "
                                      "rate (profiles/r01_pcie/fma_peak.jsonl)"}},
         "binding_roofline": {"R_pcie": r_pcie, "R_hbm": r_hbm, "R_bind": r_bind, "unit": UNIT,
-                             "frac_e2e": e2e_v / r_bind, "frac_value_vs_R_hbm": (val_v / r_hbm) if val_v else None,
+                             "frac_e2e": e2e_v / r_bind, "frac_hbm_resident_vs_R_hbm": (val_v / r_hbm) if val_v else None,
                              "pcie_measured": pc,
                              "pcie_achieved_GBps_per_dir": {
                                  "h2d": e2e_res["h2d"] / (e2e_res["device_ms_total"] / 1e3) / 1e9,

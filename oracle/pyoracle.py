@@ -15,7 +15,43 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(HERE, "liboracle.so")
-_REF = os.path.join(HERE, "_ref", "libso2dr_ref.so")
+_REF_V3 = os.path.join(HERE, "_ref", "libso2dr_ref.so")
+_REF_NATIVE = os.path.join(HERE, "_ref", "libso2dr_ref_native.so")
+_NATIVE_FLAGS = os.path.join(HERE, "_ref", "native_flags.txt")
+
+
+def _host_isa() -> set:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("flags"):
+                return {f.replace("_", "") for f in line.split(":", 1)[1].split()}
+    except OSError:
+        pass
+    return set()
+
+
+def ref_build_info() -> dict:
+    """Which reference build runs here: the -march=native build of the build host
+    (oracle/Makefile) when this CPU has every ISA extension it enabled, else the
+    portable -march=x86-64-v3 build."""
+    info = {"path": _REF_V3, "march": "x86-64-v3", "missing_isa": []}
+    try:
+        lines = [l.split() for l in open(_NATIVE_FLAGS) if l.strip()]
+    except OSError:
+        return info
+    march = next((l[1] for l in lines if l[0] == "march" and len(l) > 1), "native")
+    need = {l[0].replace("_", "") for l in lines if l[0] != "march"}
+    have = _host_isa()
+    have |= {"bmi"} if "bmi1" in have else set()
+    missing = sorted(need - have)
+    if os.path.exists(_REF_NATIVE) and not missing:
+        return {"path": _REF_NATIVE, "march": march, "missing_isa": []}
+    info["missing_isa"] = missing
+    info["native_march"] = march
+    return info
+
+
+_REF = ref_build_info()["path"]
 
 BOX, GRADIENT, STAR = 0, 1, 2
 

@@ -340,6 +340,25 @@ def _numel(a) -> int:
     return int(a.size) if isinstance(a, np.ndarray) else int(a.numel())
 
 
+def _shape(a) -> tuple:
+    return tuple(int(x) for x in a.shape)
+
+
+def _contig(a) -> bool:
+    return a.flags["C_CONTIGUOUS"] if isinstance(a, np.ndarray) else bool(a.is_contiguous())
+
+
+def _check_buf(name: str, a, cells: int, dtype_code: Optional[int] = None):
+    """The C ABI takes raw pointers: refuse a buffer whose size, dtype or layout
+    does not match what the call will read/write (an out-of-bounds DMA otherwise)."""
+    if not _contig(a):
+        raise ContractError(f"{name}: buffer must be C-contiguous")
+    if _numel(a) != cells:
+        raise ContractError(f"{name}: buffer has {_numel(a)} cells, the call needs {cells}")
+    if dtype_code is not None and _dtype_code(a) != dtype_code:
+        raise ContractError(f"{name}: dtype differs from the other buffer")
+
+
 class Engine:
     """One so2dr_ctx: a device, its streams, its HBM pool (capped by budget)."""
 
@@ -405,9 +424,7 @@ class Engine:
         if diag:
             cap = 64 + 8 * max(1, config.d) * max(1, (config.n + max(config.s_tb, 1) - 1) // max(config.s_tb, 1))
             rows = (_Diag * cap)()
-        expect = (config.sz + 2 * config.r) ** spec.dim
-        if _numel(grid) != expect:
-            raise ContractError(f"engine: grid has {_numel(grid)} cells, config needs {expect}")
+        _check_buf("engine: grid", grid, (config.sz + 2 * config.r) ** spec.dim)
         self._ck(lib().so2dr_run(self._h, MODES[mode], ctypes.byref(st), ctypes.byref(cfg),
                                  ctypes.byref(kp), ctypes.byref(hwc), ctypes.byref(hk),
                                  _dtype_code(grid), _ptr(grid), ctypes.byref(led), ctypes.byref(tim),
@@ -427,6 +444,10 @@ class Engine:
                      read: int, steps: int, tile: int, region, interior, owned) -> dict:
         st, keep = spec._c()
         rows, cols = buf0.shape
+        _check_buf("fused_kernel: buf0", buf0, rows * cols)
+        if _shape(buf1) != _shape(buf0):
+            raise ContractError(f"fused_kernel: buf1 shape {_shape(buf1)} != buf0 shape {_shape(buf0)}")
+        _check_buf("fused_kernel: buf1", buf1, rows * cols, _dtype_code(buf0))
         R = (ctypes.c_int32 * 4)(*region)
         I = (ctypes.c_int32 * 4)(*interior)
         O = (ctypes.c_int32 * 4)(*owned)
@@ -439,6 +460,10 @@ class Engine:
     def apply_step(self, spec: StencilSpec, grid_in, grid_out, row_lo: int, row_hi: int):
         st, keep = spec._c()
         sz = grid_in.shape[0] - 2 * spec.radius
+        _check_buf("apply_step: grid_in", grid_in, (sz + 2 * spec.radius) ** spec.dim)
+        if _shape(grid_out) != _shape(grid_in):
+            raise ContractError(f"apply_step: grid_out shape {_shape(grid_out)} != grid_in shape {_shape(grid_in)}")
+        _check_buf("apply_step: grid_out", grid_out, _numel(grid_in), _dtype_code(grid_in))
         self._ck(lib().so2dr_apply_step(self._h, ctypes.byref(st), _dtype_code(grid_in), sz, spec.radius,
                                         _ptr(grid_in), _ptr(grid_out), row_lo, row_hi))
         del keep
@@ -447,6 +472,7 @@ class Engine:
         st, keep = spec._c()
         out = np.empty_like(grid)
         sz = grid.shape[0] - 2 * spec.radius
+        _check_buf("run_reference: grid", grid, (sz + 2 * spec.radius) ** spec.dim)
         self._ck(lib().so2dr_run_reference(self._h, ctypes.byref(st), _dtype_code(grid), sz, spec.radius,
                                            _ptr(grid), _ptr(out), steps))
         del keep
@@ -469,6 +495,7 @@ class Engine:
         blob = ctypes.create_string_buffer(PEER_BLOB_BYTES)
         code = 0 if np.dtype(dtype) == np.float32 else 1
         self._ck(lib().so2dr_slab_prepare(self._h, ctypes.byref(st), ctypes.byref(cfg), code, rank, world, blob))
+        self._slab_rank = (rank, world)
         del keep
         return blob.raw
 
@@ -480,6 +507,9 @@ class Engine:
         cfg = config._c()
         kp = (kernel or KernelPlan(k_on=config.k_on))._c()
         led, tim = _Ledger(), _Timing()
+        rank, world = getattr(self, "_slab_rank", (0, 1))
+        lo, hi = slab_rows(config, rank, world, dim=spec.dim)
+        _check_buf("slab_run: slab", slab, (hi - lo) * (config.sz + 2 * config.r) ** (spec.dim - 1))
         self._ck(lib().so2dr_slab_run(self._h, ctypes.byref(st), ctypes.byref(cfg), ctypes.byref(kp),
                                       _dtype_code(slab), _ptr(slab), ctypes.byref(led), ctypes.byref(tim)))
         del keep

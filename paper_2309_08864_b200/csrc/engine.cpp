@@ -218,16 +218,27 @@ StencilDev make_stencil(const so2dr_stencil_desc* st) {
   if (!st->weights) throw InvalidSpecError("stencil weights are NULL");
   s.w.assign(st->weights, st->weights + n);
   bool off_axis_zero = true;
+  double wsum = 0.0;
   for (int i = 0; i < n; ++i) {
     if (!std::isfinite(s.w[i])) throw InvalidSpecError("tap weight not finite");
+    wsum += std::fabs(s.w[i]);
     const int dx = i % e - s.radius, dy = (i / e) % e - s.radius;
     const int dz = s.dim == 3 ? i / (e * e) - s.radius : 0;
     const int axes = (dz != 0) + (dy != 0) + (dx != 0);
     if (axes > 1 && s.w[i] != 0.0) off_axis_zero = false;
   }
-  // A box whose off-axis weights are all zero runs on the star kernel: the
-  // skipped taps are fma(0, v, acc) == acc for finite v (acc never -0).
-  s.kind = (st->kind == SO2DR_KIND_STAR || off_axis_zero) ? so2dr_dev::KSTAR : so2dr_dev::KBOX;
+  // A box whose off-axis weights are all zero (the reference's way to write a
+  // star, e.g. star2d1r = box(1, {0,w,0,w,w,w,0,w,0})) runs on the star kernel:
+  // the skipped taps are fma(0, v, acc) == acc whenever v is finite (and acc
+  // is never -0: the chain starts at +0). v stays finite when the input grid is
+  // finite (the API's precondition for this shortcut) and sum|w| <= 1 + 1e-6
+  // (normalised fp32 weights; |out| grows at most (1+1e-6)x per step: ~9e7
+  // steps from 1.0 to FLT_MAX). Weights that can grow the field
+  // (sum|w| > 1: it may overflow to inf, where the reference chain turns
+  // 0*inf into NaN) keep the full box chain.
+  const bool no_growth = wsum <= 1.0 + 1e-6;
+  s.kind = (st->kind == SO2DR_KIND_STAR || (off_axis_zero && no_growth)) ? so2dr_dev::KSTAR
+                                                                         : so2dr_dev::KBOX;
   if (s.kind == so2dr_dev::KSTAR)
     for (int i = 0; i < n; ++i) {
       const int dx = i % e - s.radius, dy = (i / e) % e - s.radius;
@@ -986,6 +997,39 @@ void run_resreu(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Ac
   }
 }
 
+constexpr uint32_t kSlabAbort = 0xF0000000u;  // flag value that releases every GEQ wait
+
+void abort_slab(so2dr_ctx* ctx) {
+  SlabState& sl = ctx->slab;
+  if (!sl.prepared || !sl.flags) return;
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  uint32_t* targets[] = {sl.flags, sl.flags + 1, sl.flags + 2, sl.flags + 3,
+                         sl.lower.flag, sl.lower.ack, sl.upper.flag, sl.upper.ack};
+  for (uint32_t* t : targets)
+    if (t) cuStreamWriteValue32(s, dptr(t), kSlabAbort, 0);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  cudaGetLastError();
+  sl.prepared = false;  // the connection is poisoned: prepare + connect again
+}
+
+bool slab_aborted(so2dr_ctx* ctx) {
+  SlabState& sl = ctx->slab;
+  if (!sl.prepared || !sl.flags) return false;
+  uint32_t f[4] = {0, 0, 0, 0};
+  if (cudaMemcpy(f, sl.flags, sizeof(f), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  for (uint32_t v : f)
+    if (v >= kSlabAbort) return true;
+  return false;
+}
+
 struct HostPin {
   void* base = nullptr;
   bool mine = false;
@@ -1063,15 +1107,29 @@ void run(so2dr_ctx* ctx, RunRequest& q, RunResponse& out) {
   SO2DR_CK(cudaEventRecord(ev_start, s0));
   for (int k = 1; k < nstreams; ++k) wait(ctx->stream(k), ev_start);
 
-  switch (q.mode) {
-    case SO2DR_MODE_SO2DR: run_so2dr(rc, q, cfg, acc, rec); break;
-    case SO2DR_MODE_INCORE: run_incore(rc, q, cfg, acc, rec); break;
-    case SO2DR_MODE_RESREU: run_resreu(rc, q, cfg, acc, rec); break;
+  try {
+    switch (q.mode) {
+      case SO2DR_MODE_SO2DR: run_so2dr(rc, q, cfg, acc, rec); break;
+      case SO2DR_MODE_INCORE: run_incore(rc, q, cfg, acc, rec); break;
+      case SO2DR_MODE_RESREU: run_resreu(rc, q, cfg, acc, rec); break;
+    }
+    for (int k = 1; k < nstreams; ++k) wait(s0, record_sync(ctx, ctx->stream(k)));
+    SO2DR_CK(cudaEventRecord(ev_end, s0));
+    SO2DR_CK(cudaEventSynchronize(ev_end));
+    SO2DR_CK(cudaGetLastError());
+  } catch (...) {
+    // Nothing may still write into the caller's grid (or read a host range we
+    // are about to unregister) once we return: release every flag wait (ours
+    // and, in slab mode, the neighbours' -- they then fail with "peer
+    // aborted" instead of waiting forever, cf. the reference's Gates::abort,
+    // engine.cpp:75-120) and drain all streams before HostPin unwinds.
+    abort_slab(ctx);
+    for (int k = 0; k < nstreams; ++k) cudaStreamSynchronize(ctx->stream(k));
+    cudaGetLastError();
+    throw;
   }
-  for (int k = 1; k < nstreams; ++k) wait(s0, record_sync(ctx, ctx->stream(k)));
-  SO2DR_CK(cudaEventRecord(ev_end, s0));
-  SO2DR_CK(cudaEventSynchronize(ev_end));
-  SO2DR_CK(cudaGetLastError());
+  if (q.world > 1 && slab_aborted(ctx))
+    throw ContractError("slab run: a neighbouring rank aborted its run (its error is on that rank)");
 
   float ms = 0.f;
   SO2DR_CK(cudaEventElapsedTime(&ms, ev_start, ev_end));

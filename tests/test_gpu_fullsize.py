@@ -43,7 +43,8 @@ def _windows(p, fences, h, w, rng, n_random, dim, max_windows):
     return corners + fence_boxes + rand
 
 
-def _check_fullsize(engine_budget, oracle, dim, dtype, kind, r, sz, d, s_tb, k_on, n, w, n_random, max_windows):
+def _check_fullsize(engine_budget, oracle, dim, dtype, kind, r, sz, d, s_tb, k_on, n, w, n_random, max_windows,
+                    scratch=1 << 40, every_fence=False):
     o = oracle
     eng = engine_budget
     if kind == "box":
@@ -57,9 +58,9 @@ def _check_fullsize(engine_budget, oracle, dim, dtype, kind, r, sz, d, s_tb, k_o
     eng.init_grid(sz, r, 42, dim, dtype, out=host)
     ring_before = [np.array(host[(slice(0, r),)]), np.array(host[(slice(p - r, p),)])]
     cfg = so2dr.RunConfig(sz=sz, r=r, d=d, s_tb=s_tb, k_on=k_on, n_strm=3, n=n)
-    rep = eng.run("so2dr", host, spec, cfg, so2dr.KernelPlan(k_on, 32, 1 << 40), diag=False)
+    rep = eng.run("so2dr", host, spec, cfg, so2dr.KernelPlan(k_on, 32, scratch), diag=False)
     # size-independent invariants
-    exp = so2dr.expected_ledger("so2dr", cfg, so2dr.KernelPlan(k_on, 32, 1 << 40), dim=dim, dtype=dtype)
+    exp = so2dr.expected_ledger("so2dr", cfg, so2dr.KernelPlan(k_on, 32, scratch), dim=dim, dtype=dtype)
     for k in ("htod", "dtoh", "ondevice", "kernel_invocations", "rounds"):
         assert rep.ledger[k] == exp[k], k
     assert np.array_equal(host[(slice(0, r),)], ring_before[0])
@@ -71,6 +72,14 @@ def _check_fullsize(engine_budget, oracle, dim, dtype, kind, r, sz, d, s_tb, k_o
     fences, _ = so2dr.plan_chunks(cfg)
     rng = np.random.default_rng(7)
     boxes = _windows(p, list(fences), r * s_tb, w, rng, n_random, dim, max_windows)
+    if every_fence:  # every inner fence at -h, 0 and +h (the shared region's edges)
+        h = r * s_tb
+        for f in list(fences)[1:-1]:
+            for off in (-h, 0, h):
+                y = min(max(0, f + off - w // 2), p - w)
+                for x in (0, int(rng.integers(0, p - w)), p - w):
+                    lo = (y, x) + tuple(int(rng.integers(0, p - w)) for _ in range(dim - 2))
+                    boxes.append((lo, tuple(a + w for a in lo)))
     for lo, hi in boxes:
         want = o.window_expected(lambda a, b: o.init_block(a, b, 42, dtype), sz, r, n, lo, hi, kc, wts, dim)
         got = host[tuple(slice(a, b) for a, b in zip(lo, hi))]
@@ -112,3 +121,26 @@ def test_config4_box3d1r_fullsize_slab(eng16, oracle):
 def test_config5_star2d2r_f64_fullsize(eng16, oracle):
     """BASELINE configs[4] per-GPU shape: star2d2r (j2d9pt-shaped) fp64, sz=65536 (34.4 GB), S_TB=64, k_on=4."""
     _check_fullsize(eng16, oracle, 2, np.float64, "star", 2, 65536, 16, 64, 4, 64, 32, 6, 64)
+
+
+def test_bench_workload_exact_geometry(eng16, oracle):
+    """The EXACT workload bench.py times (its constants are imported, so the test
+    follows the bench): box2d1r fp32, sz=92160 (33.98 GB host grid, 1.98x the
+    16 GiB budget), n=64, d=64, S_TB=64, k_on=4, N_strm=3, KernelPlan(k_on, 32,
+    64 MiB) -- i.e. ~1500-row K1 launches. Windows: both grid corners, every one
+    of the 63 inner fences at fence-h, fence and fence+h (h = r*S_TB, the shared
+    region's edges) at the left edge (ring columns), a random column and the right
+    edge, plus random windows; all bit-exact against the oracle's light cone."""
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    assert (bench.SZ1, bench.D_PER_RANK, bench.S_TB, bench.K_ON, bench.NSTEPS, bench.NSTRM, bench.R) == \
+        (92160, 64, 64, 4, 64, 3, 1)
+    assert bench.BUDGET == BUDGET
+    rep = _check_fullsize(eng16, oracle, 2, np.float32, "box", bench.R, bench.SZ1, bench.D_PER_RANK, bench.S_TB,
+                          bench.K_ON, bench.NSTEPS, 40, 8, 10, scratch=64 << 20, every_fence=True)
+    assert rep.timing["h2d_bytes"] == (92162 ** 2) * 4
+    assert rep.timing["kernel_launches"] == bench.D_PER_RANK * bench.S_TB // bench.K_ON

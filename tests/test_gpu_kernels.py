@@ -112,3 +112,23 @@ def test_fused_stats_match_reference(engine, oracle):
         assert rc == 0, err.value
         assert [st["scratch_load"], st["scratch_store"], st["updates"], st["redundant"]] == list(stats)
         assert (_bits(b1) == _bits(r1)).all()
+
+
+def test_growing_zero_corner_box_keeps_box_chain(engine, oracle):
+    """a box spec with zero off-axis weights whose weights can grow the
+    field (all-ones star: sum|w| = 5) must NOT take the star shortcut -- once the
+    field overflows to inf, the reference chain's fma(0, inf, acc) is NaN. 64
+    steps of 5x growth overflow fp32; the engine must match the oracle's box chain
+    (non-NaN cells bit-exact, NaN exactly where the oracle has NaN)."""
+    w = np.zeros(9)
+    w[[1, 3, 4, 5, 7]] = 1.0
+    spec = so2dr.StencilSpec.box(1, w)
+    g = oracle.init_grid(64, 1, 5, 2, np.float32)
+    want = oracle.run(g, oracle.BOX, 1, w, 64)
+    got = g.copy()
+    engine.run("incore", got, spec, so2dr.RunConfig(sz=64, r=1, d=1, s_tb=8, k_on=4, n_strm=1, n=64),
+               so2dr.KernelPlan(4, 32))
+    assert np.isnan(want).any() and np.isinf(want).any()
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    ok = ~np.isnan(want)
+    assert (_bits(got)[ok] == _bits(want)[ok]).all()
