@@ -243,6 +243,58 @@ so2dr_status so2dr_expected_ledger(so2dr_mode mode, const so2dr_run_config* cfg,
                                    const so2dr_kernel_plan* kp, int dim, so2dr_dtype dtype,
                                    uint64_t out6[6], int32_t* exact);
 
+/* ---- spec files, presets and run outputs (host-only) ----------------------
+ * RunSpecFile / parse_spec_json / parse_spec_file  proj/include/so2dr/specfile.hpp:14-28
+ * presets (--preset NAME)                          proj/tools/so2dr_main.cpp:28-68
+ * report_to_json / ledger_to_csv / diagnostics_to_csv  proj/include/so2dr/report.hpp:11-24
+ * Errors follow the reference: a syntax error is SO2DR_ERR_IO with "line L,
+ * column C" in so2dr_last_error(NULL); a missing/mistyped field names it
+ * (SO2DR_ERR_IO); an unknown kind/mode/preset or bad radius is
+ * SO2DR_ERR_INVALID_SPEC. */
+#define SO2DR_SPEC_MAX_WEIGHTS 125 /* (2r+1)^dim: box2d4r 81, 3D r=2 125 */
+typedef struct {
+  /* stencil.weights points at weights_buf of THIS struct (re-point it after
+   * copying the struct); canonical (dz, dy, dx) order, defaults filled in:
+   * box fp32(1/(2r+1)^dim), star fp32(1/(2*dim*r+1)) on axis. */
+  so2dr_stencil_desc stencil;
+  double weights_buf[SO2DR_SPEC_MAX_WEIGHTS];
+  so2dr_run_config config;
+  so2dr_kernel_plan kernel;
+  uint64_t seed;
+  int32_t mode;  /* so2dr_mode */
+  int32_t dtype; /* so2dr_dtype */
+  char stencil_name[32];     /* box2d1r, star3d1r, gradient2d, ... */
+  char hardware_path[512];   /* "" when absent */
+  char grid_dump_path[512];  /* "" when absent */
+} so2dr_spec;
+
+so2dr_status so2dr_spec_parse(const char* text, const char* origin, so2dr_spec* out);
+so2dr_status so2dr_spec_parse_file(const char* path, so2dr_spec* out);
+int so2dr_preset_count(void);
+const char* so2dr_preset_name(int i); /* NULL when out of range */
+/* Copies the preset's JSON (NUL-terminated) into buf when it fits; *len_out =
+ * its length without the NUL either way. */
+so2dr_status so2dr_preset_json(const char* name, char* buf, size_t cap, size_t* len_out);
+
+/* report.json v1 of a run, the reference's keys and order (report.cpp:21-64);
+ * modeled times come from `hw` (NULL = the B200 profile) and the ledger;
+ * `measured` (optional) adds the CUDA-event block unless deterministic. */
+typedef struct {
+  int32_t mode;          /* so2dr_mode */
+  int32_t deterministic; /* omit wall_seconds / measured */
+  const char* stencil_name;
+  so2dr_run_config config;
+  so2dr_kernel_plan kernel;
+  uint64_t checksum;
+  so2dr_ledger ledger;
+  const so2dr_hardware* hw;
+  const so2dr_timing* measured;
+} so2dr_report_in;
+so2dr_status so2dr_report_json(const so2dr_report_in* in, char* buf, size_t cap, size_t* len_out);
+so2dr_status so2dr_ledger_csv(const so2dr_ledger* ledger, char* buf, size_t cap, size_t* len_out);
+so2dr_status so2dr_diagnostics_csv(const so2dr_diag_row* rows, size_t n, char* buf, size_t cap,
+                                   size_t* len_out);
+
 #ifdef __cplusplus
 }
 #endif

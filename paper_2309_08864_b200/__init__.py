@@ -101,6 +101,13 @@ class _Timing(ctypes.Structure):
     _fields_ = TIMING_FIELDS
 
 
+class _Spec(ctypes.Structure):
+    _fields_ = [("stencil", _Stencil), ("weights_buf", ctypes.c_double * 125), ("config", _Cfg),
+                ("kernel", _KPlan), ("seed", ctypes.c_uint64), ("mode", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("stencil_name", ctypes.c_char * 32), ("hardware_path", ctypes.c_char * 512),
+                ("grid_dump_path", ctypes.c_char * 512)]
+
+
 class _Diag(ctypes.Structure):
     _fields_ = [("round", ctypes.c_int32), ("chunk", ctypes.c_int32), ("stage", ctypes.c_int32),
                 ("reserved", ctypes.c_int32), ("bytes", ctypes.c_uint64), ("updates", ctypes.c_uint64),
@@ -121,6 +128,8 @@ EXPORTS = (
     "so2dr_fused_kernel", "so2dr_apply_step", "so2dr_run_reference", "so2dr_init_grid",
     "so2dr_init_rows", "so2dr_grid_checksum", "so2dr_arena_bytes", "so2dr_device_bytes",
     "so2dr_plan_chunks", "so2dr_expected_ledger", "so2dr_kernel_stats",
+    "so2dr_spec_parse", "so2dr_spec_parse_file", "so2dr_preset_count", "so2dr_preset_name",
+    "so2dr_preset_json", "so2dr_report_json", "so2dr_ledger_csv", "so2dr_diagnostics_csv",
 )
 
 
@@ -167,8 +176,24 @@ def lib():
     L.so2dr_kernel_stats.argtypes = [i32, i32, i32, P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32),
                                      i32, i32, i64, P(u64)]
     L.so2dr_expected_ledger.argtypes = [i32, P(_Cfg), P(_KPlan), i32, i32, P(u64), P(ctypes.c_int32)]
+    cp = ctypes.c_char_p
+    L.so2dr_spec_parse.argtypes = [cp, cp, P(_Spec)]
+    L.so2dr_spec_parse_file.argtypes = [cp, P(_Spec)]
+    L.so2dr_preset_count.restype = i32
+    L.so2dr_preset_name.argtypes = [i32]
+    L.so2dr_preset_name.restype = cp
+    L.so2dr_preset_json.argtypes = [cp, cp, sz, P(sz)]
+    L.so2dr_report_json.argtypes = [P(_ReportIn), cp, sz, P(sz)]
+    L.so2dr_ledger_csv.argtypes = [P(_Ledger), cp, sz, P(sz)]
+    L.so2dr_diagnostics_csv.argtypes = [P(_Diag), sz, cp, sz, P(sz)]
     _lib = L
     return L
+
+
+class _ReportIn(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("deterministic", ctypes.c_int32), ("stencil_name", ctypes.c_char_p),
+                ("config", _Cfg), ("kernel", _KPlan), ("checksum", ctypes.c_uint64), ("ledger", _Ledger),
+                ("hw", ctypes.POINTER(_HW)), ("measured", ctypes.POINTER(_Timing))]
 
 
 def _raise(status: int, ctx=None):
@@ -439,6 +464,15 @@ class Engine:
         return RunReport(mode, config, {f: getattr(led, f) for f in LEDGER_FIELDS},
                          {f: getattr(tim, f) for f, _ in TIMING_FIELDS}, dl)
 
+    def run_spec(self, spec: "RunSpecFile", grid=None, hw: Optional[HardwareModel] = None, diag: bool = True):
+        """The CLI's `run` (proj/tools/so2dr_main.cpp:146-162) for a parsed spec
+        file / preset: init_grid(sz, r, seed) (unless `grid` is given), then
+        run_engine in place. Returns (grid, RunReport)."""
+        if grid is None:
+            grid = self.init_grid(spec.config.sz, spec.config.r, spec.seed, spec.stencil.dim, spec.dtype)
+        rep = self.run(spec.mode, grid, spec.stencil, spec.config, spec.kernel, hw, diag=diag)
+        return grid, rep
+
     # -- secondary entry points -------------------------------------------
     def fused_kernel(self, spec: StencilSpec, buf0: np.ndarray, buf1: np.ndarray, base_row: int,
                      read: int, steps: int, tile: int, region, interior, owned) -> dict:
@@ -597,3 +631,93 @@ def run_engine(mode: str, grid, spec: StencilSpec, config: RunConfig, kernel: Op
     rep = default_engine().run(mode, out, spec, config, kernel, hw, hooks)
     rep.checksum = grid_checksum(out)
     return out, rep
+
+
+# ------------------------------------ spec files, presets, run outputs --
+# proj/include/so2dr/specfile.hpp:14-28, proj/tools/so2dr_main.cpp:28-68,
+# proj/include/so2dr/report.hpp:11-24 (through the C ABI: one implementation)
+
+@dataclasses.dataclass
+class RunSpecFile:
+    """A parsed spec file / preset (RunSpecFile, specfile.hpp:14-23, plus the
+    dim/dtype/weights extensions)."""
+    stencil: StencilSpec
+    seed: int
+    mode: str
+    config: RunConfig
+    kernel: KernelPlan
+    dtype: type
+    stencil_name: str
+    hardware_path: Optional[str] = None
+    grid_dump_path: Optional[str] = None
+
+
+def _from_c_spec(c: "_Spec") -> RunSpecFile:
+    st = c.stencil
+    n = (2 * st.radius + 1) ** st.dim
+    w = np.array(c.weights_buf[:n], dtype=np.float64)
+    cfg = RunConfig(**{f: getattr(c.config, f) for f in ("sz", "r", "d", "s_tb", "k_on", "n_strm", "n", "n_a")})
+    mode = {v: k for k, v in MODES.items()}[c.mode]
+    return RunSpecFile(StencilSpec(st.kind, st.radius, st.dim, w), int(c.seed), mode, cfg,
+                       KernelPlan(c.kernel.k_on, c.kernel.tile, c.kernel.scratch_budget),
+                       np.float64 if c.dtype == 1 else np.float32, c.stencil_name.decode(),
+                       c.hardware_path.decode() or None, c.grid_dump_path.decode() or None)
+
+
+def parse_spec_json(text: str, origin: str = "spec") -> RunSpecFile:
+    c = _Spec()
+    _check(lib().so2dr_spec_parse(text.encode(), origin.encode(), ctypes.byref(c)))
+    return _from_c_spec(c)
+
+
+def parse_spec_file(path: str) -> RunSpecFile:
+    c = _Spec()
+    _check(lib().so2dr_spec_parse_file(str(path).encode(), ctypes.byref(c)))
+    return _from_c_spec(c)
+
+
+def preset_names() -> list:
+    L = lib()
+    return [L.so2dr_preset_name(i).decode() for i in range(L.so2dr_preset_count())]
+
+
+def _text(fn, *args) -> str:
+    n = ctypes.c_size_t(0)
+    _check(fn(*args, None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value + 1)
+    _check(fn(*args, buf, n.value + 1, ctypes.byref(n)))
+    return buf.value.decode()
+
+
+def preset_json(name: str) -> str:
+    return _text(lib().so2dr_preset_json, name.encode())
+
+
+def preset(name: str) -> RunSpecFile:
+    """--preset NAME: the preset's JSON through parse_spec_json (origin "preset NAME")."""
+    return parse_spec_json(preset_json(name), "preset " + name)
+
+
+def report_to_json(report: "RunReport", stencil_name: str, checksum: int, deterministic: bool = False,
+                   hw: Optional[HardwareModel] = None, kernel: Optional[KernelPlan] = None) -> str:
+    """report.json v1 (proj/src/report.cpp:21-64) of an Engine.run report."""
+    led = _Ledger(*[report.ledger[f] for f in LEDGER_FIELDS])
+    tim = _Timing(*[report.timing[f] for f, _ in TIMING_FIELDS])
+    hwc = (hw or HardwareModel())._c()
+    ri = _ReportIn(MODES[report.mode], 1 if deterministic else 0, stencil_name.encode(), report.config._c(),
+                   (kernel or KernelPlan(k_on=report.config.k_on))._c(), checksum, led, ctypes.pointer(hwc),
+                   ctypes.pointer(tim))
+    return _text(lib().so2dr_report_json, ctypes.byref(ri))
+
+
+def ledger_to_csv(ledger: dict) -> str:
+    led = _Ledger(*[ledger[f] for f in LEDGER_FIELDS])
+    return _text(lib().so2dr_ledger_csv, ctypes.byref(led))
+
+
+def diagnostics_to_csv(rows: list) -> str:
+    arr = (_Diag * max(1, len(rows)))()
+    for i, r in enumerate(rows):
+        arr[i].round, arr[i].chunk, arr[i].stage = r["round"], r["chunk"], STAGES.index(r["stage"])
+        arr[i].bytes, arr[i].updates = r["bytes"], r["updates"]
+    return _text(lib().so2dr_diagnostics_csv, arr, len(rows))

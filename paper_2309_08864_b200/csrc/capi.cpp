@@ -9,6 +9,8 @@
 #include <stdexcept>
 
 #include "engine.h"
+#include "so2dr/report.hpp"
+#include "so2dr/specfile.hpp"
 #include "so2dr/verify.hpp"
 #include "so2dr_cuda.h"
 
@@ -425,6 +427,153 @@ so2dr_status so2dr_expected_ledger(so2dr_mode mode, const so2dr_run_config* cfg,
     out6[4] = e.rounds;
     out6[5] = e.redundant_updates * (dim == 3 ? p : 1);
     if (exact) *exact = e.redundancy_exact ? 1 : 0;
+  });
+}
+
+// ---------------------------------------------------- spec files / outputs --
+
+namespace {
+
+void copy_text(char* dst, size_t cap, const std::string& src) {
+  if (!cap) return;
+  const size_t n = std::min(cap - 1, src.size());
+  std::memcpy(dst, src.data(), n);
+  dst[n] = 0;
+}
+
+void to_c_spec(const so2dr::RunSpecFile& f, so2dr_spec* out) {
+  std::memset(out, 0, sizeof(*out));
+  const int r = f.stencil.radius, dim = f.dim;
+  const int e = 2 * r + 1;
+  const int n = dim == 3 ? e * e * e : e * e;
+  if (n > SO2DR_SPEC_MAX_WEIGHTS)
+    throw so2dr::InvalidSpecError("spec: radius " + std::to_string(r) + " too large for dim " + std::to_string(dim));
+  const so2dr::StencilKind k = f.stencil.kind;
+  int kind = k == so2dr::StencilKind::gradient ? SO2DR_KIND_GRADIENT
+             : k == so2dr::StencilKind::star   ? SO2DR_KIND_STAR
+                                                : SO2DR_KIND_BOX;
+  auto on_axis = [&](int i) {
+    const int dx = i % e - r, dy = (i / e) % e - r, dz = dim == 3 ? i / (e * e) - r : 0;
+    return (dz != 0) + (dy != 0) + (dx != 0) <= 1;
+  };
+  if (kind == SO2DR_KIND_GRADIENT) {
+    // gradient ignores weights (pinned expression)
+  } else if (static_cast<int>(f.weights.size()) == n) {
+    for (int i = 0; i < n; ++i) out->weights_buf[i] = static_cast<double>(f.weights[i]);
+  } else if (!f.weights.empty()) {  // star on-axis list, canonical order
+    size_t next = 0;
+    for (int i = 0; i < n; ++i) out->weights_buf[i] = on_axis(i) ? f.weights[next++] : 0.0;
+  } else {
+    // defaults in the run's precision (stencil.cpp:27-33 for fp32 box):
+    // box 1/(2r+1)^dim, star 1/(2*dim*r+1) on axis
+    const int cnt = kind == SO2DR_KIND_STAR ? 2 * dim * r + 1 : n;
+    const double w = f.dtype == "f64" ? 1.0 / cnt : static_cast<double>(1.0f / static_cast<float>(cnt));
+    for (int i = 0; i < n; ++i) out->weights_buf[i] = (kind == SO2DR_KIND_BOX || on_axis(i)) ? w : 0.0;
+  }
+  if (f.dtype == "f32")  // fp32 runs use (float)w: store the value they will use
+    for (int i = 0; i < n; ++i) out->weights_buf[i] = static_cast<float>(out->weights_buf[i]);
+  out->stencil.kind = kind;
+  out->stencil.dim = dim;
+  out->stencil.radius = r;
+  out->stencil.weights = out->weights_buf;
+  const so2dr::RunConfig& c = f.config;
+  out->config = {c.sz, c.r, c.d, c.s_tb, c.k_on, c.n_strm, c.n, c.n_a};
+  out->kernel = {f.kernel.k_on, f.kernel.tile, f.kernel.scratch_budget};
+  out->seed = f.seed;
+  out->mode = static_cast<int32_t>(f.mode);
+  out->dtype = f.dtype == "f64" ? SO2DR_F64 : SO2DR_F32;
+  std::string name = f.stencil.name();
+  if (dim == 3) name.replace(name.find("2d"), 2, "3d");
+  copy_text(out->stencil_name, sizeof(out->stencil_name), name);
+  copy_text(out->hardware_path, sizeof(out->hardware_path), f.hardware_path.value_or(""));
+  copy_text(out->grid_dump_path, sizeof(out->grid_dump_path), f.grid_dump_path.value_or(""));
+}
+
+void out_text(const std::string& s, char* buf, size_t cap, size_t* len_out) {
+  if (len_out) *len_out = s.size();
+  if (buf && cap > s.size()) {
+    std::memcpy(buf, s.data(), s.size());
+    buf[s.size()] = 0;
+  }
+}
+
+}  // namespace
+
+so2dr_status so2dr_spec_parse(const char* text, const char* origin, so2dr_spec* out) {
+  return guard(nullptr, [&] {
+    if (!text || !out) throw so2dr::ContractError("spec_parse: text/out is NULL");
+    to_c_spec(so2dr::parse_spec_json(text, origin ? origin : "spec"), out);
+  });
+}
+
+so2dr_status so2dr_spec_parse_file(const char* path, so2dr_spec* out) {
+  return guard(nullptr, [&] {
+    if (!path || !out) throw so2dr::ContractError("spec_parse_file: path/out is NULL");
+    to_c_spec(so2dr::parse_spec_file(path), out);
+  });
+}
+
+int so2dr_preset_count(void) { return static_cast<int>(so2dr::preset_names().size()); }
+
+const char* so2dr_preset_name(int i) {
+  static const std::vector<std::string> names = so2dr::preset_names();
+  return i >= 0 && i < static_cast<int>(names.size()) ? names[i].c_str() : nullptr;
+}
+
+so2dr_status so2dr_preset_json(const char* name, char* buf, size_t cap, size_t* len_out) {
+  return guard(nullptr, [&] {
+    if (!name) throw so2dr::ContractError("preset_json: name is NULL");
+    out_text(so2dr::preset_json(name), buf, cap, len_out);
+  });
+}
+
+so2dr_status so2dr_report_json(const so2dr_report_in* in, char* buf, size_t cap, size_t* len_out) {
+  return guard(nullptr, [&] {
+    if (!in) throw so2dr::ContractError("report_json: input is NULL");
+    so2dr::RunReport rep;
+    rep.mode = static_cast<so2dr::EngineMode>(in->mode);
+    rep.config = to_cfg(&in->config);
+    rep.kernel = to_kp(&in->kernel);
+    rep.stencil_name = in->stencil_name ? in->stencil_name : "";
+    rep.checksum = in->checksum;
+    const so2dr_ledger& l = in->ledger;
+    rep.ledger = so2dr::LedgerSnapshot{l.htod,          l.dtoh,          l.ondevice,
+                                       l.scratch_load,  l.scratch_store, l.element_updates,
+                                       l.redundant_updates, l.kernel_invocations, l.rounds};
+    rep.times = so2dr::modeled_times(rep.ledger, to_hw(in->hw));
+    rep.transfer_time_excluded = rep.mode == so2dr::EngineMode::incore;
+    if (in->measured) {
+      const so2dr_timing& t = *in->measured;
+      rep.arena_peak = t.arena_peak;
+      rep.arena_capacity = t.arena_capacity;
+      rep.wall_seconds = t.wall_seconds;
+      rep.measured = so2dr::MeasuredTimes{t.device_ms, t.kernel_ms, t.kernel_launches, t.kernel_alg_bytes,
+                                          t.device_bytes};
+    }
+    out_text(so2dr::report_to_json(rep, in->deterministic != 0), buf, cap, len_out);
+  });
+}
+
+so2dr_status so2dr_ledger_csv(const so2dr_ledger* l, char* buf, size_t cap, size_t* len_out) {
+  return guard(nullptr, [&] {
+    if (!l) throw so2dr::ContractError("ledger_csv: ledger is NULL");
+    out_text(so2dr::ledger_to_csv(so2dr::LedgerSnapshot{l->htod, l->dtoh, l->ondevice, l->scratch_load,
+                                                        l->scratch_store, l->element_updates,
+                                                        l->redundant_updates, l->kernel_invocations,
+                                                        l->rounds}),
+             buf, cap, len_out);
+  });
+}
+
+so2dr_status so2dr_diagnostics_csv(const so2dr_diag_row* rows, size_t n, char* buf, size_t cap,
+                                   size_t* len_out) {
+  return guard(nullptr, [&] {
+    if (n && !rows) throw so2dr::ContractError("diagnostics_csv: rows is NULL");
+    std::vector<so2dr::DiagRow> v;
+    for (size_t i = 0; i < n; ++i)
+      v.push_back({rows[i].round, rows[i].chunk, static_cast<so2dr::Stage>(rows[i].stage), rows[i].bytes,
+                   rows[i].updates});
+    out_text(so2dr::diagnostics_to_csv(v), buf, cap, len_out);
   });
 }
 

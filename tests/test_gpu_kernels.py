@@ -128,7 +128,7 @@ def test_growing_zero_corner_box_keeps_box_chain(engine, oracle):
     got = g.copy()
     engine.run("incore", got, spec, so2dr.RunConfig(sz=64, r=1, d=1, s_tb=8, k_on=4, n_strm=1, n=64),
                so2dr.KernelPlan(4, 32))
-    assert np.isnan(want).any() and np.isinf(want).any()
+    assert np.isnan(want).any()  # overflowed to inf, then 0*inf = NaN spread
     assert np.array_equal(np.isnan(got), np.isnan(want))
     ok = ~np.isnan(want)
     assert (_bits(got)[ok] == _bits(want)[ok]).all()
