@@ -18,7 +18,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libso2dr_b200.so")
+# SO2DR_LIB: load an experiment build instead (tools/build_variant.sh)
+LIB_PATH = os.environ.get("SO2DR_LIB") or os.path.join(HERE, "libso2dr_b200.so")
 
 # ---------------------------------------------------------------- errors --
 # proj/include/so2dr/errors.hpp:11-63

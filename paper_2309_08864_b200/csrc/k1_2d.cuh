@@ -71,6 +71,9 @@ struct K1Args2D {
   int cpb;          // cp.async piece bytes (16/8/4): largest dividing the pitch
   unsigned* counter;  // work-item counter (zeroed before the launch)
   T w[81];          // (2R+1)^2 weights, canonical order
+  // fp32 r <= 2: packed weight pairs {w(d, dx), w(d-1, dx)} for d = 1-R..R at
+  // [(d+R-1)(2R+1) + dx+R], read by the fast path's FFMA2 from uniform registers
+  uint64_t wp[20];
 };
 
 template <typename T>
@@ -199,9 +202,12 @@ __device__ __forceinline__ void issue_inrow(void* dst, const void* src) {
 template <typename T, int R, int S, int KIND, int V, int NT>
 struct K1Plan2D {
   // prefetch ring depth (rows per lane; power of two; <= 32 KB of smem)
-  static constexpr int RING = (V * (int)sizeof(T)) <= 16 ? 8 : 4;
+  static constexpr int RING = (V * (int)sizeof(T)) <= 16 ? 16 : 8;
   static constexpr int E = 2 * R + 1;
   static constexpr int H = R * S;
+  // strip halo in columns: H rounded up to whole lanes, so every lane is
+  // either entirely inside the strip's output columns or entirely halo
+  static constexpr int HS = (H + V - 1) / V * V;
   static constexpr int NW = NT / 32;
   static constexpr int CPB = (V * (int)sizeof(T)) >= 16 ? 16 : V * (int)sizeof(T);  // copy bytes
   static constexpr int VEC = CPB / (int)sizeof(T);  // elements per copy / alignment unit
@@ -217,15 +223,15 @@ template <typename T, int R, int S, int KIND, int V, int NT, bool SCALAR = false
 __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
                                         T (&ring)[K1Plan2D<T, R, S, KIND, V, NT>::RING][NT * V]) {
   using P = K1Plan2D<T, R, S, KIND, V, NT>;
-  constexpr int E = P::E, H = P::H, VEC = P::VEC, CPB = P::CPB;
+  constexpr int E = P::E, H = P::H, VEC = P::VEC;
   constexpr int kRing = P::RING;
   const int tid = threadIdx.x, lane = tid & 31;
   constexpr bool live = true;
 
   // ---- warp geometry ------------------------------------------------------
   const int wc0 = a.xorg + wx * a.strip;  // column of lane 0 cell 0
-  const int OX0 = max(wc0 + H, a.x0);
-  const int OX1 = min(wc0 + H + a.strip, a.x1);
+  const int OX0 = max(wc0 + P::HS, a.x0);
+  const int OX1 = min(wc0 + P::HS + a.strip, a.x1);
   const int OY0 = a.y0 + sg * a.seg;
   const int OY1 = min(OY0 + a.seg, a.y1);
   const int sy0 = a.base, sy1 = a.base + a.rows;
@@ -485,252 +491,6 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
   cp_async_wait<0>();
 }
 
-// ---------------------------------------------------------------------------
-// Packed fp32 variant for box / star: identical pipeline, but every carried
-// value lives in 64-bit register pairs holding cells (k, k + V/2) of the
-// lane, and every multiply-add is an FFMA2 (fma.rn.f32x2). With this pairing
-// the operand pair of every tap, (s[k+dx], s[k+V/2+dx]), is either a pair the
-// previous stage emitted as-is or one of the 2R pairs formed with a shuffled
-// halo value, so the FMA pipe spends its cycles on FFMA2, not on register
-// moves (each FMA-pipe instruction costs 2 issue cycles per SMSP; FFMA2 does
-// 64 fmas in them, a scalar FFMA 32). Each half is an IEEE round-to-nearest
-// fma: results are bit-identical to the scalar chain.
-template <int R, int S, int KIND, int V, int NT, bool HYB = false>
-__device__ __forceinline__ void k1_item_pk(const K1Args2D<float>& a, int wx, int sg,
-                                           float (&ring)[K1Plan2D<float, R, S, KIND, V, NT>::RING][NT * V]) {
-  using T = float;
-  using P = K1Plan2D<T, R, S, KIND, V, NT>;
-  constexpr int E = P::E, H = P::H, VEC = P::VEC;
-  constexpr int kRing = P::RING;
-  constexpr int HV = V / 2;
-  // Accumulator ring of M = 2R+2 slots (output row y in slot y mod M), one more
-  // than the 2R+1 rows a consumed row touches. With 2R+1 slots the slot stage u
-  // reads (stage u-1's emission of the previous iteration) is the slot stage
-  // u-1 restarts in the same iteration, a register WAR inside the iteration;
-  // with the extra slot the read slot is not written in that iteration
-  // (measured +14% at k_on 1-2, +-2% at 4-8: profiles/r01_k1).
-  constexpr int M = E + 1;
-  constexpr int NP = HV + 2 * R;  // operand pairs per consumed row
-  static_assert(V % 2 == 0 && KIND != KGRAD, "packed path: box/star, even V");
-  const int tid = threadIdx.x, lane = tid & 31;
-  constexpr bool live = true;
-  const int wc0 = a.xorg + wx * a.strip;
-  const int OX0 = max(wc0 + H, a.x0);
-  const int OX1 = min(wc0 + H + a.strip, a.x1);
-  const int OY0 = a.y0 + sg * a.seg;
-  const int OY1 = min(OY0 + a.seg, a.y1);
-  const int sy0 = a.base, sy1 = a.base + a.rows;
-  const int lo0 = max(OY0 - H, sy0), hi0 = min(OY1 + H, sy1);
-  const int n_iter = OY1 - lo0 + S * (R + 1);
-  const int xt = wc0 + lane * V;
-
-  int lo[S + 1], hi[S + 1];
-#pragma unroll
-  for (int u = 0; u <= S; ++u) {
-    lo[u] = max(OY0 - R * (S - u), sy0);
-    hi[u] = min(OY1 + R * (S - u), sy1);
-  }
-  unsigned ringmask = 0, smask = 0;
-#pragma unroll
-  for (int k = 0; k < V; ++k) {
-    const int x = xt + k;
-    if (x < a.ix0 || x >= a.ix1) ringmask |= 1u << k;
-    if (live && x >= OX0 && x < OX1) smask |= 1u << k;
-  }
-  unsigned lmask = 0;
-#pragma unroll
-  for (int v = 0; v < V; v += VEC)
-    if (xt + v >= 0 && xt + v < a.pitch) lmask |= 1u << v;
-  const bool warp_ring = wc0 < a.ix0 || wc0 + 32 * V > a.ix1;
-
-  // cell k of a packed row: pair k % HV, half k / HV
-  auto cell = [](const uint64_t (&p)[HV], int k) SO2DR_INLINE -> float {
-    float lo, hi;
-    unpack2(p[k % HV], lo, hi);
-    return k < HV ? lo : hi;
-  };
-
-  // Stage u's emitted row is never copied: it stays in its accumulator slot,
-  // which stage u+1 reads in the next iteration before stage u re-initialises
-  // it (stages run in descending order). Only stage 0 has its own row.
-  uint64_t cp0[HV];        // stage 0 (loaded) row, packed
-  uint64_t ap[S][M][HV];   // partial accumulators, packed
-#pragma unroll
-  for (int k = 0; k < HV; ++k) cp0[k] = 0ull;
-#pragma unroll
-  for (int u = 0; u < S; ++u)
-#pragma unroll
-    for (int e = 0; e < M; ++e)
-#pragma unroll
-      for (int k = 0; k < HV; ++k) ap[u][e][k] = 0ull;
-
-  T* my_ring = &ring[0][tid * V];
-  const T* src_col = a.in + xt;
-  auto issue = [&](int row) SO2DR_INLINE {
-    const bool ok = row < hi0;
-    T* dst = my_ring + (row & (kRing - 1)) * (NT * V);
-    const T* src = src_col + (int64_t)(row - sy0) * a.pitch;
-    const int cpb = row_cpb(a.in + (int64_t)(row - sy0) * a.pitch);  // warp-uniform
-#pragma unroll
-    for (int v = 0; v < V; v += VEC)
-      if (ok) issue_vec<T, VEC>(dst + v, src + v, cpb, xt + v, a.pitch);
-    cp_async_commit();
-  };
-  // steady state: the strip owns no column outside the interior; addressing
-  // off a running row offset (off = (row0 - sy0) * pitch, see k1_item)
-  int64_t off = (int64_t)(lo0 - sy0) * a.pitch;
-  const T* ld_lane = src_col + (int64_t)(kRing - 1) * a.pitch;
-  T* st_lane = a.out + xt - (int64_t)(S * (R + 1)) * a.pitch;
-  auto issue_fast = [&](int row) SO2DR_INLINE {
-    if (row < hi0) issue_inrow<V * (int)sizeof(T)>(my_ring + (row & (kRing - 1)) * (NT * V), ld_lane + off);
-    cp_async_commit();
-  };
-#pragma unroll
-  for (int d = 0; d < kRing - 1; ++d) issue(lo0 + d);
-
-  auto passthru = [&](int row, int k) SO2DR_INLINE -> T {
-    const int x = xt + k;
-    if (x < 0 || x >= a.cols) return T(0);
-    return __ldg(a.in + (int64_t)(row - sy0) * a.pitch + x);
-  };
-
-  auto body = [&](auto phase_tag, auto fast_tag, int it) SO2DR_INLINE {
-    constexpr int PH = decltype(phase_tag)::value;
-    constexpr bool FAST = decltype(fast_tag)::value;
-    const int row0 = lo0 + it;
-#pragma unroll
-    for (int u = S; u >= 1; --u) {
-      const int A = row0 - u - (u - 1) * R;
-      const int Erow = A - R;
-      const bool consume = FAST || (A >= lo[u - 1] && A < hi[u - 1]);
-      const bool emit = FAST || (Erow >= lo[u] && Erow < hi[u]);
-
-      // the consumed row: stage u-1's emission of the previous iteration
-      uint64_t in[HV];
-#pragma unroll
-      // stage u-1 emitted it last iteration into slot (PH - 1 - 2R) mod M
-      constexpr int rd_slot = (PH - 1 - 2 * R + 2 * M) % M;
-      for (int k = 0; k < HV; ++k) in[k] = (u == 1) ? cp0[k] : ap[u >= 2 ? u - 2 : 0][rd_slot][k];
-      // halo values (lanes 0/31 get their own: strip-edge garbage, never output)
-      float hl[R], hr[R];
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        hl[j] = __shfl_up_sync(0xffffffffu, cell(in, V - R + j), 1);
-        hr[j] = __shfl_down_sync(0xffffffffu, cell(in, j), 1);
-      }
-      // s_i: i < R halo-left, R <= i < R+V own cell i-R, else halo-right
-      auto sval = [&](int i) SO2DR_INLINE -> float {
-        if (i < R) return hl[i];
-        if (i < R + V) return cell(in, i - R);
-        return hr[i - R - V];
-      };
-      uint64_t op[NP];  // op[j] = (s_j, s_{j+HV})
-#pragma unroll
-      for (int j = 0; j < NP; ++j)
-        op[j] = (HYB || (j >= R && j < R + HV)) ? (j >= R && j < R + HV ? in[j - R] : 0ull)
-                                                : pack2(sval(j), sval(j + HV));
-      // one tap: FFMA2 on an in-register pair, or (HYB) two scalar FFMAs on
-      // the halves when the operand pair would need a shuffled halo value
-      auto tap = [&](float w, int j, uint64_t x) SO2DR_INLINE -> uint64_t {
-        if (!HYB || (j >= R && j < R + HV)) return fma2p(w, op[j], x);
-        float xl, xh;
-        unpack2(x, xl, xh);
-        return pack2(__fmaf_rn(w, sval(j), xl), __fmaf_rn(w, sval(j + HV), xh));
-      };
-
-      if (consume) {
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-          const int dy = m - R;
-          const int sl = (PH - m + 2 * M) % M;
-#pragma unroll
-          for (int k = 0; k < HV; ++k) {
-            uint64_t x = (m == 0) ? 0ull : ap[u - 1][sl][k];
-            if constexpr (KIND == KBOX) {
-#pragma unroll
-              for (int dx = -R; dx <= R; ++dx) x = tap(a.w[(dy + R) * E + dx + R], R + k + dx, x);
-            } else if (dy != 0) {
-              x = tap(a.w[(dy + R) * E + R], R + k, x);
-            } else {
-#pragma unroll
-              for (int dx = -R; dx <= R; ++dx) x = tap(a.w[R * E + dx + R], R + k + dx, x);
-            }
-            ap[u - 1][sl][k] = x;
-          }
-        }
-      }
-      if (emit) {
-        constexpr int se = (PH - 2 * R + 2 * M) % M;
-        uint64_t outp[HV];
-#pragma unroll
-        for (int k = 0; k < HV; ++k) outp[k] = ap[u - 1][se][k];
-        if constexpr (!FAST) {
-          const bool ring_row = Erow < a.iy0 || Erow >= a.iy1;
-          if (ring_row || ringmask) {
-            float v[V];
-#pragma unroll
-            for (int k = 0; k < V; ++k) {
-              v[k] = cell(outp, k);
-              if (ring_row || (ringmask & (1u << k))) v[k] = passthru(Erow, k);
-            }
-#pragma unroll
-            for (int k = 0; k < HV; ++k) ap[u - 1][se][k] = outp[k] = pack2(v[k], v[k + HV]);
-          }
-        }
-        if (u == S) {
-          T* dst = FAST ? st_lane + off : a.out + (int64_t)(Erow - sy0) * a.pitch + xt;
-#pragma unroll
-          for (int k = 0; k < V; ++k)
-            if (smask & (1u << k)) dst[k] = cell(outp, k);
-        }
-      }
-    }
-    if constexpr (FAST)
-      issue_fast(row0 + kRing - 1);
-    else
-      issue(row0 + kRing - 1);
-    cp_async_wait<kRing - 1>();
-    if (FAST || row0 < hi0) {
-      const T* src = my_ring + (row0 & (kRing - 1)) * (NT * V);
-#pragma unroll
-      for (int k = 0; k < HV; ++k) cp0[k] = pack2(src[k], src[k + HV]);
-    }
-    off += a.pitch;
-  };
-
-  int f_lo = 0, f_hi = hi0 - lo0;
-#pragma unroll
-  for (int u = 1; u <= S; ++u) {
-    const int c = lo0 - u - (u - 1) * R;
-    f_lo = max(f_lo, lo[u - 1] - c);
-    f_hi = min(f_hi, hi[u - 1] - c);
-    f_lo = max(f_lo, max(lo[u], a.iy0) + R - c);
-    f_hi = min(f_hi, min(hi[u], a.iy1) + R - c);
-  }
-  if (warp_ring) f_hi = f_lo;
-
-  int it = 0;
-  auto run_general = [&](int stop) SO2DR_INLINE {
-    while (it < stop) {
-      [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
-        ((it < stop ? (body(std::integral_constant<int, Ps>{}, std::false_type{}, it), ++it, void())
-                    : void()),
-         ...);
-      }(std::make_integer_sequence<int, M>{});
-    }
-  };
-  const int fl = (f_lo + M - 1) / M * M;
-  if (f_hi - fl >= M) {
-    run_general(fl);
-    while (it + M <= f_hi) {
-      [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
-        ((body(std::integral_constant<int, Ps>{}, std::true_type{}, it), ++it), ...);
-      }(std::make_integer_sequence<int, M>{});
-    }
-  }
-  run_general(n_iter);
-  cp_async_wait<0>();
-}
 
 // Work item -> (strip, segment). The strips that own ring columns run the
 // general (range-checked) path for their whole height and cost several times
@@ -752,12 +512,23 @@ __device__ __forceinline__ void k1_item_coords(const K1Args2D<T>& a, int item, i
   }
 }
 
-// Persistent warps with dynamic work distribution: every warp of a
-// one-wave grid fetches (strip, segment) items from an atomic counter, so the
-// SMs stay busy until the last item (no partial last wave).
-template <typename T, int R, int S, int KIND, int V, int NT, int MINB, bool SCALAR = false>
+}  // namespace so2dr_dev
+
+#include "k1_2d_stream.cuh"
+
+namespace so2dr_dev {
+
+// Persistent warps with dynamic work distribution: every warp of a one-wave
+// grid fetches (strip, segment) items from an atomic counter, so the SMs stay
+// busy until the last item (no partial last wave). Items that touch no
+// pass-through cell run the branch-free streaming path (k1_2d_stream.cuh);
+// the others the range-checked general path (k1_item). The last warp to
+// leave re-arms the counter pair for the next launch that uses it, so no
+// memset is enqueued per launch.
+template <typename T, int R, int S, int KIND, int V, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
   __shared__ __align__(16) T ring[K1Plan2D<T, R, S, KIND, V, NT>::RING][NT * V];
+  constexpr int H = R * S;
   const int lane = threadIdx.x & 31;
   const int total = a.warps_x * a.nseg;
   for (;;) {
@@ -767,23 +538,37 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
     if (item >= total) break;
     int wx, sg;
     k1_item_coords(a, item, wx, sg);
-    k1_item<T, R, S, KIND, V, NT, SCALAR>(a, wx, sg, ring);
+    // fp64 r >= 3: the streaming path's 2C+1 accumulator pairs of 4 doubles
+    // outgrow the register file (spills); those shapes keep the general path
+    if constexpr (KIND != KGRAD && !(sizeof(T) == 8 && R >= 3)) {
+      const int wc0 = a.xorg + wx * a.strip;
+      const int OY0 = a.y0 + sg * a.seg;
+      const int OY1 = min(OY0 + a.seg, a.y1);
+      // rows stage 1 emits (the widest stage range) all interior, no ring column
+      const int lo1 = max(OY0 - (H - R), a.base), hi1 = min(OY1 + (H - R), a.base + a.rows);
+      // inner: no pass-through cell, even pitch (8-byte aligned rows), and the
+      // strip's output columns start / end on lane boundaries
+      constexpr int HS = K1Plan2D<T, R, S, KIND, V, NT>::HS;
+      const int OX0 = max(wc0 + HS, a.x0), OX1 = min(wc0 + HS + a.strip, a.x1);
+      const bool lanes_whole = OX0 >= OX1 || ((OX0 - wc0) % V == 0 && (OX1 - wc0) % V == 0);
+      const bool inner = wc0 >= a.ix0 && wc0 + 32 * V <= a.ix1 && lo1 >= a.iy0 && hi1 <= a.iy1 &&
+                         (a.pitch & 1) == 0 && lanes_whole;
+      if (inner)
+        k1_item_stream<T, R, S, KIND, V, NT, false>(a, wx, sg, ring);
+      else
+        k1_item_stream<T, R, S, KIND, V, NT, true>(a, wx, sg, ring);
+    } else {
+      k1_item<T, R, S, KIND, V, NT, true>(a, wx, sg, ring);
+    }
   }
-}
-
-template <int R, int S, int KIND, int V, int NT, int MINB, bool HYB = false>
-__global__ void __launch_bounds__(NT, MINB) k1_stencil2d_pk(const K1Args2D<float> a) {
-  __shared__ __align__(16) float ring[K1Plan2D<float, R, S, KIND, V, NT>::RING][NT * V];
-  const int lane = threadIdx.x & 31;
-  const int total = a.warps_x * a.nseg;
-  for (;;) {
-    int item = 0;
-    if (lane == 0) item = static_cast<int>(atomicAdd(a.counter, 1u));
-    item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= total) break;
-    int wx, sg;
-    k1_item_coords(a, item, wx, sg);
-    k1_item_pk<R, S, KIND, V, NT, HYB>(a, wx, sg, ring);
+  if (lane == 0) {
+    __threadfence();
+    const unsigned nw = gridDim.x * (NT / 32);
+    if (atomicAdd(a.counter + 1, 1u) == nw - 1) {
+      a.counter[0] = 0u;
+      a.counter[1] = 0u;
+      __threadfence();
+    }
   }
 }
 

@@ -5,22 +5,23 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
 
 #include "k1_launch.h"
 
 namespace so2dr_dev {
 
 int device_sm_count() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int n = 0;
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
-      n = 148;
-    cached = n;
+  static std::atomic<int> cached[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  int n = cached[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cached[dev].store(n, std::memory_order_relaxed);
   }
-  return cached;
+  return n;
 }
 
 int k1_max_steps(int dim, int dtype, int kind, int radius) {
@@ -28,8 +29,8 @@ int k1_max_steps(int dim, int dtype, int kind, int radius) {
     if (kind == KGRAD) return radius == 1 ? 8 : 0;
     if (radius < 1 || radius > 4) return 0;
     // must match maxs2d() in k1_2d_impl.cuh
-    if (dtype == 0) return radius == 1 ? 8 : radius == 2 ? 4 : radius == 3 ? 2 : 1;
-    return radius == 1 ? 8 : radius == 2 ? 4 : 1;
+    if (dtype == 0) return radius == 1 ? 8 : 4;
+    return radius == 1 ? 8 : radius == 2 ? 4 : radius == 3 ? 2 : 1;
   }
   if (dim == 3) {
     if (kind == KGRAD) return 0;
@@ -103,25 +104,33 @@ cudaError_t launch_init(int dtype, void* out, int64_t pitch, int p, int dim, int
 }  // namespace so2dr_dev
 
 // ---- work counters for the persistent K1 kernels ---------------------------
-// A ring of device counters per device; each launch takes the next slot and
-// zeroes it on its own stream first. A slot is reused only 65536 launches
-// later, long after the earlier launch finished.
+// One counter pair per (device, stream): [0] hands out work items, [1] counts
+// the warps that left. The last warp of a launch re-arms both (k1_stencil2d),
+// so launches on one stream -- which never overlap -- reuse the pair without
+// a per-launch memset. Device globals start zeroed at module load.
 namespace so2dr_dev {
-constexpr unsigned kCounters = 65536;
-__device__ unsigned g_k1_counters[kCounters];
+constexpr unsigned kCounterPairs = 4096;
+__device__ unsigned g_k1_counters[2 * kCounterPairs];
 
 unsigned* k1_next_counter(cudaStream_t stream) {
+  static std::mutex mu;
   static unsigned* base[64] = {};
-  static std::atomic<unsigned> next{0};
+  static std::unordered_map<uint64_t, unsigned> slots;
+  static unsigned used[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
   if (!base[dev]) {
     void* p = nullptr;
     if (cudaGetSymbolAddress(&p, g_k1_counters) != cudaSuccess) return nullptr;
     base[dev] = static_cast<unsigned*>(p);
   }
-  unsigned* slot = base[dev] + (next.fetch_add(1) % kCounters);
-  if (cudaMemsetAsync(slot, 0, sizeof(unsigned), stream) != cudaSuccess) return nullptr;
-  return slot;
+  const uint64_t key = (static_cast<uint64_t>(dev) << 56) ^ reinterpret_cast<uintptr_t>(stream);
+  auto it = slots.find(key);
+  if (it == slots.end()) {
+    if (used[dev] >= kCounterPairs) return nullptr;  // more live streams than pairs
+    it = slots.emplace(key, used[dev]++).first;
+  }
+  return base[dev] + 2 * it->second;
 }
 }  // namespace so2dr_dev

@@ -1,8 +1,8 @@
-"""Every fp32 K1 variant must stay bit-exact with the oracle: the default
-scalar-FFMA pipeline, the packed FFMA2 kernel (SO2DR_K1_IMPL=pk), the hybrid
-FFMA2/FFMA kernel (SO2DR_K1_IMPL=hyb) and the
-paired-strip kernel (SO2DR_K1_IMPL=p2, S = 3..4). Run in a subprocess: the
-variant is chosen once per process."""
+"""K1 results must not depend on how a launch is cut into work items: the
+same so2dr runs with 1, 3 and 16 items per resident warp (SO2DR_K1_IPW: long
+segments vs many short ones, i.e. different mixes of inner / edge items and of
+pipeline fills) stay bit-exact with the oracle. Run in a subprocess: the knob
+is read once per process."""
 import os
 import subprocess
 import sys
@@ -22,7 +22,7 @@ import pyoracle as o
 eng = so2dr.Engine(0)
 for kind, w, spec in (("box", o.box_weights(1), so2dr.StencilSpec.box(1)),
                       ("star", o.star_weights(1), so2dr.StencilSpec.star(1))):
-    for sz, d, s_tb, k, n in ((300, 3, 8, 4, 12), (517, 1, 6, 3, 9), (1000, 4, 16, 4, 20)):
+    for sz, d, s_tb, k, n in ((300, 3, 8, 4, 12), (517, 1, 6, 3, 9), (1000, 4, 16, 4, 20), (1536, 4, 16, 8, 16)):
         if sz % d:
             continue
         g = eng.init_grid(sz, 1, 7)
@@ -34,12 +34,12 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("impl", ["p2", "pk", "hyb", "default"])
-def test_k1_variant_bit_exact(impl):
+@pytest.mark.parametrize("ipw", ["1", "3", "16", "default"])
+def test_k1_segmentation_bit_exact(ipw):
     env = dict(os.environ)
-    env.pop("SO2DR_K1_IMPL", None)
-    if impl != "default":
-        env["SO2DR_K1_IMPL"] = impl
+    env.pop("SO2DR_K1_IPW", None)
+    if ipw != "default":
+        env["SO2DR_K1_IPW"] = ipw
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
