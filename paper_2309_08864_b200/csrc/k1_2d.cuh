@@ -68,7 +68,9 @@ struct K1Args2D {
   int warps_x;      // strips along x
   int nseg;         // row segments; work items = warps_x * nseg
   int nl, nr;       // leading / trailing strips that own ring columns (slow path)
+  int gnl, gnr;     // the same in strip groups (CTA items of the streaming path)
   int cpb;          // cp.async piece bytes (16/8/4): largest dividing the pitch
+  int aligned8;     // both buffers 8-byte aligned and the pitch even (rows 8-byte aligned)
   unsigned* counter;  // work-item counter (zeroed before the launch)
   T w[81];          // (2R+1)^2 weights, canonical order
   // fp32 r <= 2: packed weight pairs {w(d, dx), w(d-1, dx)} for d = 1-R..R at
@@ -131,6 +133,30 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// ---- mbarrier + bulk copy (TMA engine) helpers -----------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_addr(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (16-byte aligned, multiple of 16 bytes) that
+// completes `bytes` on the mbarrier
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
 }
 
 // Copy the VEC consecutive elements at column x of one row, global -> shared,
@@ -213,15 +239,27 @@ struct K1Plan2D {
   static constexpr int VEC = CPB / (int)sizeof(T);  // elements per copy / alignment unit
   static_assert(V % VEC == 0, "V must be a whole number of copy vectors");
   static_assert(R <= V, "warp-shuffle halo needs R <= V");
+  // shared memory: NW per-warp cp.async rings (RING rows x 32 lanes x V),
+  // aliased by the CTA bulk-copy ring of the streaming path (RING/2 slots x 2
+  // rows x the strip group's columns + one 16-byte slack chunk); the CTA only
+  // switches between the two at item boundaries (__syncthreads)
+  static constexpr int LANE_RING_B = RING * 32 * V * (int)sizeof(T);
+  static constexpr int GROUP_COLS = NW * (32 * V - 2 * HS) + 2 * HS;  // NW strips incl. halo
+  static constexpr int CTA_ROWB = (GROUP_COLS * (int)sizeof(T) + 16 + 15) / 16 * 16;
+  static constexpr int SMEM_B = ((NW * LANE_RING_B > RING * CTA_ROWB ? NW * LANE_RING_B : RING * CTA_ROWB) + 127) / 128 * 128;
+  // HBM-bound depths (S <= 2) stream through the CTA bulk-copy ring in strip
+  // groups; the FMA-bound depths keep per-warp items (lockstep warps of a
+  // group contend for the FMA pipe: 1701 vs 2184 GCell/s at box2d1r k=4,
+  // profiles/r02_k1)
+  static constexpr bool GROUPED = S <= 2;
   static constexpr int NACC = (KIND == KGRAD) ? 0 : S;
   static constexpr int NGR = (KIND == KGRAD) ? S : 0;
 };
 
-// One work item = (strip wx, row segment sg) processed by one warp; `ring` is
-// the calling CTA's shared ring (each lane uses its own slots only).
+// One work item = (strip wx, row segment sg) processed by one warp; `wring`
+// is the warp's shared ring (each lane uses its own slots only).
 template <typename T, int R, int S, int KIND, int V, int NT, bool SCALAR = false>
-__device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
-                                        T (&ring)[K1Plan2D<T, R, S, KIND, V, NT>::RING][NT * V]) {
+__device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg, T* wring) {
   using P = K1Plan2D<T, R, S, KIND, V, NT>;
   constexpr int E = P::E, H = P::H, VEC = P::VEC;
   constexpr int kRing = P::RING;
@@ -274,11 +312,11 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
     for (int k = 0; k < V; ++k) cur[u][k] = T(0);
 
   // ---- prefetch (each lane reads back only what it copied: no barrier) ------
-  T* my_ring = &ring[0][tid * V];
+  T* my_ring = wring + lane * V;
   const T* src_col = a.in + xt;
   auto issue = [&](int row) SO2DR_INLINE {
     const bool ok = row < hi0;  // rows below lo0 never requested
-    T* dst = my_ring + (row & (kRing - 1)) * (NT * V);
+    T* dst = my_ring + (row & (kRing - 1)) * (32 * V);
     const T* src = src_col + (int64_t)(row - sy0) * a.pitch;
     const int cpb = row_cpb(a.in + (int64_t)(row - sy0) * a.pitch);  // warp-uniform
 #pragma unroll
@@ -293,7 +331,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
   const T* ld_lane = src_col + (int64_t)(kRing - 1) * a.pitch;
   T* st_lane = a.out + xt - (int64_t)(S * (R + 1)) * a.pitch;
   auto issue_fast = [&](int row) SO2DR_INLINE {
-    if (row < hi0) issue_inrow<V * (int)sizeof(T)>(my_ring + (row & (kRing - 1)) * (NT * V), ld_lane + off);
+    if (row < hi0) issue_inrow<V * (int)sizeof(T)>(my_ring + (row & (kRing - 1)) * (32 * V), ld_lane + off);
     cp_async_commit();
   };
 #pragma unroll
@@ -448,7 +486,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
       issue(row0 + kRing - 1);
     cp_async_wait<kRing - 1>();
     if (FAST || row0 < hi0) {
-      const T* src = my_ring + (row0 & (kRing - 1)) * (NT * V);
+      const T* src = my_ring + (row0 & (kRing - 1)) * (32 * V);
 #pragma unroll
       for (int k = 0; k < V; ++k) cur[0][k] = src[k];
     }
@@ -498,17 +536,20 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg,
 // fetched last they left one SM running alone for ~25% of the launch
 // (profiles/r01_baseline/k1_full.json: SM active avg 73.5% of elapsed).
 template <typename T>
-__device__ __forceinline__ void k1_item_coords(const K1Args2D<T>& a, int item, int& wx, int& sg) {
-  const int ne = a.nl + a.nr;
+__device__ __forceinline__ void k1_item_coords(const K1Args2D<T>& a, int item, int& wx, int& sg, int units) {
+  // units: strips (per-warp items) or strip groups (CTA items); the leading /
+  // trailing units that own ring columns come first
+  const int nl = units == a.warps_x ? a.nl : a.gnl, nr = units == a.warps_x ? a.nr : a.gnr;
+  const int ne = nl + nr;
   if (item < ne * a.nseg) {
     sg = item / ne;
     const int j = item - sg * ne;
-    wx = j < a.nl ? j : a.warps_x - ne + j;
+    wx = j < nl ? j : units - ne + j;
   } else {
-    const int inner = a.warps_x - ne;
+    const int inner = units - ne;
     const int i = item - ne * a.nseg;
     sg = i / inner;
-    wx = a.nl + (i - sg * inner);
+    wx = nl + (i - sg * inner);
   }
 }
 
@@ -527,47 +568,130 @@ namespace so2dr_dev {
 // memset is enqueued per launch.
 template <typename T, int R, int S, int KIND, int V, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
-  __shared__ __align__(16) T ring[K1Plan2D<T, R, S, KIND, V, NT>::RING][NT * V];
+  using P = K1Plan2D<T, R, S, KIND, V, NT>;
+  constexpr int NW = NT / 32;
   constexpr int H = R * S;
-  const int lane = threadIdx.x & 31;
-  const int total = a.warps_x * a.nseg;
-  for (;;) {
-    int item = 0;
-    if (lane == 0) item = static_cast<int>(atomicAdd(a.counter, 1u));
-    item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= total) break;
-    int wx, sg;
-    k1_item_coords(a, item, wx, sg);
-    // fp64 r >= 3: the streaming path's 2C+1 accumulator pairs of 4 doubles
-    // outgrow the register file (spills); those shapes keep the general path
-    if constexpr (KIND != KGRAD && !(sizeof(T) == 8 && R >= 3)) {
+  __shared__ __align__(128) unsigned char smem[P::SMEM_B];
+  __shared__ __align__(8) uint64_t bars[2][P::RING / 2];
+  __shared__ int s_item;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T* wring = reinterpret_cast<T*>(smem + warp * P::LANE_RING_B);
+  // streaming shapes (fp32 / fp64 r <= 2): the fp64 r >= 3 streaming state
+  // outgrows the register file, so those (and the gradient) stay per warp
+  constexpr bool kStream = KIND != KGRAD && !(sizeof(T) == 8 && R >= 3);
+  if constexpr (kStream && P::GROUPED) {
+    // CTA work items = (strip group of NW strips, row segment)
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int i = 0; i < P::RING / 2; ++i) {
+        mbar_init(&bars[0][i], 1);   // full: the issuing lane's expect_tx
+        mbar_init(&bars[1][i], NW);  // empty: one release per warp
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    GroupRing gr;
+    gr.ring_s = smem_u32(smem);
+    gr.ring = reinterpret_cast<const char*>(smem);
+    gr.full_s = smem_u32(&bars[0][0]);
+    gr.empty_s = smem_u32(&bars[1][0]);
+    gr.rowb = P::CTA_ROWB;
+    unsigned g_it = 0;  // CTA-ring slots consumed (identical in every warp)
+    const int groups = (a.warps_x + NW - 1) / NW;
+    const int total = groups * a.nseg;
+    for (;;) {
+      __syncthreads();  // every warp done with the previous item (and s_item)
+      if (threadIdx.x == 0) s_item = static_cast<int>(atomicAdd(a.counter, 1u));
+      __syncthreads();
+      const int item = s_item;
+      if (item >= total) break;
+      int gx, sg;
+      k1_item_coords(a, item, gx, sg, groups);
+      const int wx0 = gx * NW;
+      const int wc0 = a.xorg + wx0 * a.strip;
+      const int OY0 = a.y0 + sg * a.seg;
+      const int OY1 = min(OY0 + a.seg, a.y1);
+      // inner group: NW whole strips, no pass-through cell, rows stage 1 emits
+      // (the widest stage range) all interior, 8-byte aligned rows, output
+      // columns on lane boundaries, and the bulk copy's 16-byte slack inside
+      // the row
+      const int lo1 = max(OY0 - (H - R), a.base), hi1 = min(OY1 + (H - R), a.base + a.rows);
+      const int wce = wc0 + (NW - 1) * a.strip + 32 * V;  // group's end column
+      const int OX0 = max(wc0 + P::HS, a.x0), OX1 = min(wce - P::HS, a.x1);
+      const bool lanes_whole = OX0 >= OX1 || ((OX0 - wc0) % V == 0 && (OX1 - wc0) % V == 0);
+      const bool inner = wx0 + NW <= a.warps_x && wc0 >= a.ix0 && wce <= a.ix1 && lo1 >= a.iy0 &&
+                         hi1 <= a.iy1 && wce * (int)sizeof(T) + 16 <= a.cols * (int)sizeof(T) && a.aligned8 &&
+                         lanes_whole;
+      if (inner) {
+        gr.wcg = wc0;
+        k1_item_stream<T, R, S, KIND, V, NT, kModeGroup>(a, wx0 + warp, sg, wring, gr, g_it);
+      } else if (wx0 + warp < a.warps_x) {
+        k1_item_stream<T, R, S, KIND, V, NT, kModeEdge>(a, wx0 + warp, sg, wring, gr, g_it);
+      }
+    }
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(a.counter + 1, 1u) == gridDim.x - 1) {
+        a.counter[0] = 0u;
+        a.counter[1] = 0u;
+        __threadfence();
+      }
+    }
+  } else if constexpr (kStream) {
+    // per-warp work items = (strip, row segment) on the streaming path
+    GroupRing gr{};
+    unsigned g_it = 0;
+    const int total = a.warps_x * a.nseg;
+    for (;;) {
+      int item = 0;
+      if (lane == 0) item = static_cast<int>(atomicAdd(a.counter, 1u));
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= total) break;
+      int wx, sg;
+      k1_item_coords(a, item, wx, sg, a.warps_x);
       const int wc0 = a.xorg + wx * a.strip;
       const int OY0 = a.y0 + sg * a.seg;
       const int OY1 = min(OY0 + a.seg, a.y1);
-      // rows stage 1 emits (the widest stage range) all interior, no ring column
       const int lo1 = max(OY0 - (H - R), a.base), hi1 = min(OY1 + (H - R), a.base + a.rows);
-      // inner: no pass-through cell, even pitch (8-byte aligned rows), and the
-      // strip's output columns start / end on lane boundaries
-      constexpr int HS = K1Plan2D<T, R, S, KIND, V, NT>::HS;
-      const int OX0 = max(wc0 + HS, a.x0), OX1 = min(wc0 + HS + a.strip, a.x1);
+      const int OX0 = max(wc0 + P::HS, a.x0), OX1 = min(wc0 + P::HS + a.strip, a.x1);
       const bool lanes_whole = OX0 >= OX1 || ((OX0 - wc0) % V == 0 && (OX1 - wc0) % V == 0);
-      const bool inner = wc0 >= a.ix0 && wc0 + 32 * V <= a.ix1 && lo1 >= a.iy0 && hi1 <= a.iy1 &&
-                         (a.pitch & 1) == 0 && lanes_whole;
+      const bool inner = wc0 >= a.ix0 && wc0 + 32 * V <= a.ix1 && lo1 >= a.iy0 && hi1 <= a.iy1 && a.aligned8 &&
+                         lanes_whole;
       if (inner)
-        k1_item_stream<T, R, S, KIND, V, NT, false>(a, wx, sg, ring);
+        k1_item_stream<T, R, S, KIND, V, NT, kModeLane>(a, wx, sg, wring, gr, g_it);
       else
-        k1_item_stream<T, R, S, KIND, V, NT, true>(a, wx, sg, ring);
-    } else {
-      k1_item<T, R, S, KIND, V, NT, true>(a, wx, sg, ring);
+        k1_item_stream<T, R, S, KIND, V, NT, kModeEdge>(a, wx, sg, wring, gr, g_it);
     }
-  }
-  if (lane == 0) {
-    __threadfence();
-    const unsigned nw = gridDim.x * (NT / 32);
-    if (atomicAdd(a.counter + 1, 1u) == nw - 1) {
-      a.counter[0] = 0u;
-      a.counter[1] = 0u;
+    if (lane == 0) {
       __threadfence();
+      const unsigned nw = gridDim.x * NW;
+      if (atomicAdd(a.counter + 1, 1u) == nw - 1) {
+        a.counter[0] = 0u;
+        a.counter[1] = 0u;
+        __threadfence();
+      }
+    }
+  } else {
+    // per-warp work items = (strip, row segment): general path
+    const int total = a.warps_x * a.nseg;
+    for (;;) {
+      int item = 0;
+      if (lane == 0) item = static_cast<int>(atomicAdd(a.counter, 1u));
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= total) break;
+      int wx, sg;
+      k1_item_coords(a, item, wx, sg, a.warps_x);
+      k1_item<T, R, S, KIND, V, NT, true>(a, wx, sg, wring);
+    }
+    // The last warp to leave re-arms the counter pair for the next launch
+    // that uses it (no memset per launch).
+    if (lane == 0) {
+      __threadfence();
+      const unsigned nw = gridDim.x * NW;
+      if (atomicAdd(a.counter + 1, 1u) == nw - 1) {
+        a.counter[0] = 0u;
+        a.counter[1] = 0u;
+        __threadfence();
+      }
     }
   }
 }

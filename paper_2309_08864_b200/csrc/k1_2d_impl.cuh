@@ -40,7 +40,7 @@ constexpr int maxs2d(int R) {
 template <typename T>
 constexpr int minb2d(int R, int S) {
   if (SO2DR_K1_MINB > 0) return SO2DR_K1_MINB;
-  if (sizeof(T) == 4 && R == 1) return S <= 3 ? 4 : S == 4 ? 3 : 2;
+  if (sizeof(T) == 4 && R == 1) return S <= 2 ? 4 : S <= 4 ? 3 : 2;
   return 1;
 }
 
@@ -91,6 +91,8 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   {
     const int64_t pb = L.pitch * static_cast<int64_t>(sizeof(T));
     a.cpb = pb % 16 == 0 ? 16 : pb % 8 == 0 ? 8 : 4;
+    a.aligned8 = pb % 8 == 0 && reinterpret_cast<uintptr_t>(L.in) % 8 == 0 &&
+                 reinterpret_cast<uintptr_t>(L.out) % 8 == 0;
   }
   // one warp = one independent strip of 32*V columns, 2H of them halo
   constexpr int HS = P::HS;  // H rounded up to whole lanes
@@ -110,6 +112,10 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
       a.nl = a.warps_x;
       a.nr = 0;
     }
+    const int groups = (a.warps_x + NT / 32 - 1) / (NT / 32);
+    a.gnl = (a.nl + NT / 32 - 1) / (NT / 32);
+    a.gnr = std::max(0, groups - (a.warps_x - a.nr) / (NT / 32));  // incl. a partial last group
+    if (a.gnl + a.gnr >= groups) a.gnl = groups, a.gnr = 0;
   }
   constexpr int NW = NT / 32;
   const int height = L.y1 - L.y0;
@@ -129,14 +135,19 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   const int resident_warps = sms * occ * NW;
   const int min_seg = std::max(32, 4 * (2 * H + 2 * S * ((R + 1) / 2)));
   const int max_ns = std::max(1, height / min_seg);
-  int ns = std::max(1, (k1_items_per_warp(height) * resident_warps + a.warps_x - 1) / a.warps_x);
+  // streaming shapes hand out CTA items (strip groups of NW strips), the
+  // general path warp items (strips)
+  constexpr bool kGroup = KIND != KGRAD && !(sizeof(T) == 8 && R >= 3) && P::GROUPED;
+  const int units = kGroup ? (a.warps_x + NW - 1) / NW : a.warps_x;
+  const int workers = kGroup ? sms * occ : resident_warps;
+  int ns = std::max(1, (k1_items_per_warp(height) * workers + units - 1) / units);
   ns = std::min(ns, max_ns);
   a.seg = (height + ns - 1) / ns;
   a.nseg = (height + a.seg - 1) / a.seg;
   a.counter = k1_next_counter(stream);
   if (!a.counter) return cudaErrorUnknown;
-  const int items = a.warps_x * a.nseg;
-  const int ctas = std::max(1, std::min(sms * occ, (items + NW - 1) / NW));
+  const int items = units * a.nseg;
+  const int ctas = std::max(1, std::min(sms * occ, kGroup ? items : (items + NW - 1) / NW));
   kern<<<ctas, NT, 0, stream>>>(a);
   return cudaGetLastError();
 }

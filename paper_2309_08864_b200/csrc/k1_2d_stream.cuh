@@ -151,18 +151,52 @@ __device__ __forceinline__ void store_lane_pred(T* dst, const T (&v)[V], unsigne
 // the completed rows' ring cells (ring rows: all cells; ring columns: the
 // lane's ring cells) are reset to the read buffer's value, which is the value
 // of a pass-through cell at every step; loads are range-checked per element.
-template <typename T, int R, int S, int KIND, int V, int NT, bool EDGE>
-__device__ __forceinline__ void k1_item_stream(const K1Args2D<T>& a, int wx, int sg,
-                                               T (&ring)[K1Plan2D<T, R, S, KIND, V, NT>::RING][NT * V]) {
+//
+// Stage-0 rows. Inner items are processed by the whole CTA: its NW warps take
+// NW adjacent strips of the same segment (a strip group), and the group's
+// rows stream through a CTA ring filled by bulk copies (the TMA engine:
+// cp.async.bulk + a `full` mbarrier per slot, tx-counted). One copy per row
+// covers all NW strips (from the 16-byte-aligned address at or below the
+// group's first column; rows that start 8 bytes off copy one extra chunk),
+// so the lanes issue no per-lane copy instructions and the L2 sees
+// whole-sector requests. The copy of iteration j is issued by warp j mod NW,
+// PF iterations ahead, after every warp released the slot's previous use
+// (an `empty` mbarrier with one arrival per warp). Each lane reads its V
+// cells with two 8-byte LDS. EDGE items run per warp and keep per-lane
+// range-checked cp.async (lanes may hang over the grid).
+struct GroupRing {
+  unsigned ring_s;   // shared address of the CTA ring (slot = 2 rows of rowb bytes)
+  const char* ring;  // generic address of the same
+  unsigned full_s;   // RING/2 `full` mbarriers (8 bytes apart)
+  unsigned empty_s;  // RING/2 `empty` mbarriers
+  unsigned rowb;     // bytes per ring row (16-byte multiple)
+  int wcg;           // column of the group's first strip (lane 0 cell 0 of warp 0)
+};
+
+// Item modes: the stage-0 load path and the pass-through handling.
+enum : int {
+  kModeEdge = 0,   // per warp; pass-through cells; range-checked per-lane cp.async
+  kModeLane = 1,   // per warp, inner; 8-byte per-lane cp.async (the FMA-bound depths)
+  kModeGroup = 2,  // CTA strip group, inner; bulk-copy CTA ring (the HBM-bound depths)
+};
+
+template <typename T, int R, int S, int KIND, int V, int NT, int MODE>
+__device__ __forceinline__ void k1_item_stream(const K1Args2D<T>& a, int wx, int sg, T* wring, const GroupRing& gr,
+                                               unsigned& g_it) {
   using P = K1Plan2D<T, R, S, KIND, V, NT>;
   using SP = StreamPlan2D<T, R, KIND>;
   constexpr int E = 2 * R + 1, H = R * S;
   constexpr int C = SP::C, NS = SP::NSLOT;
   constexpr int RING_IT = P::RING / 2;  // ring depth in iterations (2 rows each)
-  constexpr int PF = RING_IT - 1;       // prefetch distance (iterations)
+  // prefetch distance: the lane ring refills the slot read one iteration
+  // earlier; the CTA ring leaves one slot of slack between the slowest warp's
+  // release and the refill
+  constexpr bool EDGE = MODE == kModeEdge, GROUP = MODE == kModeGroup;
+  constexpr int PF = GROUP ? RING_IT - 2 : RING_IT - 1;
+  constexpr int NW = NT / 32;
   static_assert(P::RING % 2 == 0 && RING_IT >= 2, "ring holds whole row pairs");
   static_assert(KIND != KGRAD, "fast path: box / star");
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   const int wc0 = a.xorg + wx * a.strip;
   const int OX0 = max(wc0 + P::HS, a.x0);
@@ -197,39 +231,77 @@ __device__ __forceinline__ void k1_item_stream(const K1Args2D<T>& a, int wx, int
       if (m & (1u << k)) v[k] = __ldg(g + k);
   };
 
-  // ---- stage-0 rows through the per-lane cp.async ring ----------------------
-  // (each lane reads back only what it copied: no barrier). ldp = the first
-  // row of the pair the next issue fetches; stp = the first stored row.
-  T* my_ring = &ring[0][tid * V];
-  const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(my_ring));
-  constexpr unsigned ROWB = NT * V * sizeof(T);  // one ring row (all lanes)
+  // ---- stage-0 rows ---------------------------------------------------------
+  // (EDGE: per-lane cp.async ring in the warp's region, each lane reads back
+  // only what it copied; inner: the CTA bulk-copy ring). ldp / bsrc = the
+  // lane's / the group's first cell of the next row pair.
+  T* my_ring = wring + lane * V;
+  const unsigned ring_s = smem_u32(my_ring);
+  constexpr unsigned ROWB = 32 * V * sizeof(T);  // one lane-ring row (32 lanes)
   const int64_t pitch2 = 2 * a.pitch;
   const T* ldp = a.in + xt + (int64_t)(lo0 - sy0) * a.pitch;
+  // inner: byte offset of the group's first cell past the 16-byte boundary,
+  // for the pair's first / second row (fixed per item: 2 rows = 16k bytes)
+  const T* grp0 = a.in + gr.wcg + (int64_t)(lo0 - sy0) * a.pitch;
+  const unsigned off0 = static_cast<unsigned>(reinterpret_cast<uintptr_t>(grp0)) & 15u;
+  const unsigned off1 = static_cast<unsigned>(reinterpret_cast<uintptr_t>(grp0 + a.pitch)) & 15u;
+  const unsigned gbytes = (NW * a.strip + 32 * V - a.strip) * sizeof(T);  // group row bytes
+  const unsigned nb0 = (gbytes + off0 + 15u) & ~15u, nb1 = (gbytes + off1 + 15u) & ~15u;
+  const T* bsrc = grp0;
+  const unsigned g0 = g_it;
+  // read cursors: slot address, its `full` barrier, phase parity
+  unsigned rd_f = gr.full_s + 8u * (g0 % RING_IT);
+  unsigned rd_s = gr.ring_s + (g0 % RING_IT) * 2u * gr.rowb;
+  unsigned rd_par = (g0 / RING_IT) & 1u;
+  const unsigned f_end = gr.full_s + 8u * RING_IT;
+  const unsigned lane_off = (wc0 - gr.wcg) * sizeof(T) + lane * V * sizeof(T);
+  if constexpr (GROUP) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   auto issue = [&](int it) SO2DR_INLINE {
     const int row = lo0 + 2 * it;
-    const unsigned d = ring_s + ((2 * it) & (P::RING - 1)) * ROWB;
-    if (EDGE && warp_ring) {  // lanes may hang over the padded grid
-      T* dg = my_ring + ((2 * it) & (P::RING - 1)) * (NT * V);
-#pragma unroll
-      for (int r2 = 0; r2 < 2; ++r2)
-        if (row + r2 < hi0) {
-          const T* gr = ldp + (int64_t)r2 * a.pitch;
-          const int cpb = row_cpb(gr - xt);
-#pragma unroll
-          for (int v = 0; v < V; v += P::VEC)
-            issue_vec<T, P::VEC>(dg + r2 * NT * V + v, gr + v, cpb, xt + v, a.pitch);
-        }
-    } else if constexpr (!EDGE) {
-      // inner items need an even pitch (checked by the caller): every row
-      // start is 8-byte aligned, so 8-byte pieces need no alignment test
-      cp_lane8<V * (int)sizeof(T)>(d, ldp, row < hi0);
-      cp_lane8<V * (int)sizeof(T)>(d + ROWB, ldp + a.pitch, row + 1 < hi0);
+    if constexpr (GROUP) {
+      if (it < n_iter && (it & (NW - 1)) == warp) {  // warp-uniform: the whole warp stays converged
+        const unsigned gj = g0 + it, slot = gj % RING_IT;
+        // the slot's previous use released by every warp (first use: parity 1 passes)
+        mbar_wait_addr(gr.empty_s + 8u * slot, ((gj / RING_IT) & 1u) ^ 1u);
+        const unsigned fb = gr.full_s + 8u * slot, dst = gr.ring_s + slot * 2u * gr.rowb;
+        const unsigned n0 = row < hi0 ? nb0 : 0u, n1 = row + 1 < hi0 ? nb1 : 0u;
+        // lane 0 arms the barrier and issues the row copies (predicated, no branch)
+        asm volatile(
+            "{\n .reg .pred p, p0, p1;\n setp.eq.u32 p, %7, 0;\n"
+            " setp.ne.and.u32 p0, %3, 0, p;\n setp.ne.and.u32 p1, %5, 0, p;\n"
+            " @p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%6], %8;\n"
+            " @p0 cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%6];\n"
+            " @p1 cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%1], [%4], %5, [%6];\n}\n" ::"r"(dst),
+            "r"(dst + gr.rowb), "l"(reinterpret_cast<const char*>(bsrc) - off0), "r"(n0),
+            "l"(reinterpret_cast<const char*>(bsrc + a.pitch) - off1), "r"(n1), "r"(fb), "r"(lane), "r"(n0 + n1)
+            : "memory");
+      }
+      bsrc += pitch2;
     } else {
-      cp_lane_pred<V * (int)sizeof(T)>(d, ldp, row < hi0);
-      cp_lane_pred<V * (int)sizeof(T)>(d + ROWB, ldp + a.pitch, row + 1 < hi0);
+      const unsigned d = ring_s + ((2 * it) & (P::RING - 1)) * ROWB;
+      if constexpr (MODE == kModeLane) {
+        // inner strips need 8-byte aligned rows (checked by the caller): no
+        // alignment test, 8-byte pieces
+        cp_lane8<V * (int)sizeof(T)>(d, ldp, row < hi0);
+        cp_lane8<V * (int)sizeof(T)>(d + ROWB, ldp + a.pitch, row + 1 < hi0);
+      } else if (warp_ring) {  // lanes may hang over the padded grid
+        T* dg = my_ring + ((2 * it) & (P::RING - 1)) * (32 * V);
+#pragma unroll
+        for (int r2 = 0; r2 < 2; ++r2)
+          if (row + r2 < hi0) {
+            const T* gr2 = ldp + (int64_t)r2 * a.pitch;
+            const int cpb = row_cpb(gr2 - xt);
+#pragma unroll
+            for (int v = 0; v < V; v += P::VEC)
+              issue_vec<T, P::VEC>(dg + r2 * 32 * V + v, gr2 + v, cpb, xt + v, a.pitch);
+          }
+      } else {
+        cp_lane_pred<V * (int)sizeof(T)>(d, ldp, row < hi0);
+        cp_lane_pred<V * (int)sizeof(T)>(d + ROWB, ldp + a.pitch, row + 1 < hi0);
+      }
+      cp_async_commit();
+      ldp += pitch2;
     }
-    cp_async_commit();
-    ldp += pitch2;
   };
 #pragma unroll
   for (int i = 0; i < PF; ++i) issue(i);
@@ -249,14 +321,42 @@ __device__ __forceinline__ void k1_item_stream(const K1Args2D<T>& a, int wx, int
   auto body = [&](auto phase_tag, int it) SO2DR_INLINE {
     constexpr int PH = decltype(phase_tag)::value;
     issue(it + PF);
-    cp_async_wait<PF>();
     T in0[2][V];
-    {
-      const T* src = my_ring + ((2 * it) & (P::RING - 1)) * (NT * V);  // (LDS.128 x 2)
+    if constexpr (GROUP) {
+      mbar_wait_addr(rd_f, rd_par);
+      const char* r0 = gr.ring + (rd_s - gr.ring_s) + off0 + lane_off;
+      const char* r1 = r0 + gr.rowb + (off1 - off0);
+      T x[2][V];
+#pragma unroll
+      for (int k = 0; k < V; k += 8 / (int)sizeof(T)) {  // 8-byte LDS (rows start 8-byte aligned)
+        if constexpr (sizeof(T) == 4) {
+          const float2 x0 = *reinterpret_cast<const float2*>(r0 + 4 * k);
+          const float2 x1 = *reinterpret_cast<const float2*>(r1 + 4 * k);
+          x[0][k] = x0.x, x[0][k + 1] = x0.y, x[1][k] = x1.x, x[1][k + 1] = x1.y;
+        } else {
+          x[0][k] = *reinterpret_cast<const T*>(r0 + 8 * k);
+          x[1][k] = *reinterpret_cast<const T*>(r1 + 8 * k);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) in0[0][k] = x[0][k], in0[1][k] = x[1][k];
+      // release the slot: every lane's LDS above is ordered before lane 0's
+      // arrive (__syncwarp orders the warp's accesses; arrive is a release)
+      __syncwarp();
+      asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %1, 0;\n @p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n}\n" ::"r"(
+                       gr.empty_s + (rd_f - gr.full_s)),
+                   "r"(lane)
+                   : "memory");
+      rd_f += 8u;
+      rd_s += 2u * gr.rowb;
+      if (rd_f == f_end) rd_f = gr.full_s, rd_s = gr.ring_s, rd_par ^= 1u;
+    } else {
+      cp_async_wait<PF>();
+      const T* src = my_ring + ((2 * it) & (P::RING - 1)) * (32 * V);
 #pragma unroll
       for (int k = 0; k < V; ++k) in0[0][k] = src[k];
 #pragma unroll
-      for (int k = 0; k < V; ++k) in0[1][k] = src[NT * V + k];
+      for (int k = 0; k < V; ++k) in0[1][k] = src[32 * V + k];
     }
     constexpr int SC = (PH - C + NS) % NS;  // slot completed this iteration
 
@@ -337,7 +437,8 @@ __device__ __forceinline__ void k1_item_stream(const K1Args2D<T>& a, int wx, int
       ((it < n_iter ? (body(std::integral_constant<int, Ps>{}, it), ++it, void()) : void()), ...);
     }(std::make_integer_sequence<int, NS>{});
   }
-  cp_async_wait<0>();
+  if constexpr (GROUP) g_it += n_iter;  // every issued slot was waited on
+  else cp_async_wait<0>();
 }
 
 }  // namespace so2dr_dev
