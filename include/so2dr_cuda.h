@@ -229,6 +229,11 @@ so2dr_status so2dr_kernel_stats(int radius, int steps, int tile, const int32_t r
                                 int sy1, int64_t cols, uint64_t stats_out[4]);
 so2dr_status so2dr_arena_bytes(const so2dr_run_config* cfg, const so2dr_kernel_plan* kp,
                                uint64_t* out);
+/* Largest step count one K1 launch fuses for (dim, dtype, kind, radius): the
+ * engine splits a longer fused_kernel call (the reference's kernels.cpp:80-109
+ * runs any s <= k_on in one tiled pass) into launches of at most this many
+ * steps. 0 = shape unsupported. No GPU needed. */
+int32_t so2dr_k1_max_steps(int dim, so2dr_dtype dtype, so2dr_kind kind, int radius);
 /* Real device footprint of an so2dr run (2 buffers per stream + slots + pools). */
 so2dr_status so2dr_device_bytes(const so2dr_run_config* cfg, int dim, so2dr_dtype dtype,
                                 uint64_t* out);

@@ -127,7 +127,7 @@ EXPORTS = (
     "so2dr_host_alloc", "so2dr_host_free",
     "so2dr_slab_rows", "so2dr_slab_prepare", "so2dr_slab_connect", "so2dr_slab_run",
     "so2dr_fused_kernel", "so2dr_apply_step", "so2dr_run_reference", "so2dr_init_grid",
-    "so2dr_init_rows", "so2dr_grid_checksum", "so2dr_arena_bytes", "so2dr_device_bytes",
+    "so2dr_init_rows", "so2dr_grid_checksum", "so2dr_arena_bytes", "so2dr_device_bytes", "so2dr_k1_max_steps",
     "so2dr_plan_chunks", "so2dr_expected_ledger", "so2dr_kernel_stats",
     "so2dr_spec_parse", "so2dr_spec_parse_file", "so2dr_preset_count", "so2dr_preset_name",
     "so2dr_preset_json", "so2dr_report_json", "so2dr_ledger_csv", "so2dr_diagnostics_csv",
@@ -606,6 +606,12 @@ def arena_bytes(config: RunConfig, kernel: KernelPlan) -> int:
     out = ctypes.c_uint64()
     _check(lib().so2dr_arena_bytes(ctypes.byref(config._c()), ctypes.byref(kernel._c()), ctypes.byref(out)))
     return out.value
+
+
+def k1_max_steps(dim: int, dtype, kind: int, radius: int) -> int:
+    """Largest step count one K1 launch fuses (longer calls are split); 0 = unsupported."""
+    code = 0 if np.dtype(dtype) == np.float32 else 1
+    return int(lib().so2dr_k1_max_steps(dim, code, kind, radius))
 
 
 def device_bytes(config: RunConfig, dim: int = 2, dtype=np.float32) -> int:

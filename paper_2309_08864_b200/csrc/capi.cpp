@@ -9,6 +9,7 @@
 #include <stdexcept>
 
 #include "engine.h"
+#include "k1_launch.h"
 #include "so2dr/report.hpp"
 #include "so2dr/specfile.hpp"
 #include "so2dr/verify.hpp"
@@ -378,6 +379,10 @@ so2dr_status so2dr_arena_bytes(const so2dr_run_config* cfg, const so2dr_kernel_p
     if (!out) throw so2dr::ContractError("arena_bytes: out is NULL");
     *out = so2dr::so2dr_arena_bytes(to_cfg(cfg), to_kp(kp));
   });
+}
+
+int32_t so2dr_k1_max_steps(int dim, so2dr_dtype dtype, so2dr_kind kind, int radius) {
+  return so2dr_dev::k1_max_steps(dim, dtype == SO2DR_F64 ? 1 : 0, kind, radius);
 }
 
 so2dr_status so2dr_device_bytes(const so2dr_run_config* cfg, int dim, so2dr_dtype dtype,

@@ -26,11 +26,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <utility>
 
 #include "k1_2d.cuh"  // fma_rn, cp_async helpers
 #include "k1_launch.h"
+
+#ifndef SO2DR_K3D_SHAPE  // fp32 radius-1 cells per thread: 22 = 2x2 on 512 threads, 24 = 2x4 on 256
+#define SO2DR_K3D_SHAPE 22
+#endif
 
 namespace so2dr_dev {
 
@@ -49,45 +52,40 @@ struct K1Args3D {
   int tile_x, tile_y;    // valid output cells per CTA along x / y
   int xorg, yorg;        // origin of CTA (0,0)'s thread cell (aligned)
   int cpb;               // cp.async piece bytes (largest of 16/8/4 dividing the pitch)
+  int nx, ny, nz;        // tiles along x / y, z segments (work items nx*ny*nz)
+  unsigned* counter;     // work-item counter pair (k1_next_counter)
   T w[125];              // (2R+1)^3 canonical weights
 };
 
+// One CTA work item (x-y tile, z segment). Every iteration runs the same
+// body, including the pipeline fill and drain (as the 2D streaming path,
+// k1_2d_stream.cuh): a plane a stage computes from planes outside its light
+// cone never reaches a stored plane. Pass-through cells (ring planes / rows /
+// columns): after every stage the emitted plane's ring cells are reset to the
+// read buffer's value (a CTA-uniform test per plane); tiles that hang over the
+// padded grid load with per-element range checks.
 template <typename T, int R, int S, int KIND, int V, int VY, int NT>
-__global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
+__device__ __forceinline__ void k1_tile3d(const K1Args3D<T>& a, int tx, int ty, int tz, unsigned char* smem_raw) {
   constexpr int E = 2 * R + 1, H = R * S, NW = NT / 32;
   constexpr int RING = 4;
-  constexpr int CPB = (V * (int)sizeof(T)) >= 16 ? 16 : V * (int)sizeof(T);
-  constexpr int VEC = CPB / (int)sizeof(T);
-  static_assert(R <= V && R <= VY, "halo must come from the neighbouring thread only");
-
-  // dynamic shared memory: input ring [RING][VY][NT*V], then the y-halo
-  // exchange [parity][stage][warp+1][top/bottom][R][32*V] (+2 guard warps)
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   using Ring = T[RING][VY][NT * V];
   using YEdge = T[2][S][NW + 2][2][R][32 * V];
   Ring& ring = *reinterpret_cast<Ring*>(smem_raw);
   YEdge& yedge = *reinterpret_cast<YEdge*>(smem_raw + sizeof(Ring));
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cx0 = a.xorg + blockIdx.x * a.tile_x;  // x of lane 0 cell 0
-  const int cy0 = a.yorg + blockIdx.y * a.tile_y;  // y of warp 0 row 0
+  const int cx0 = a.xorg + tx * a.tile_x;  // x of lane 0 cell 0
+  const int cy0 = a.yorg + ty * a.tile_y;  // y of warp 0 row 0
   const int xt = cx0 + lane * V;
   const int yt = cy0 + warp * VY;
-  const int OZ0 = a.z0 + blockIdx.z * a.seg;
+  const int OZ0 = a.z0 + tz * a.seg;
   const int OZ1 = min(OZ0 + a.seg, a.z1);
   const int sz0 = a.base, sz1 = a.base + a.planes;
   const int lo0 = max(OZ0 - H, sz0), hi0 = min(OZ1 + H, sz1);
   const int n_iter = OZ1 - lo0 + S * (R + 1);
-  // valid output window of this CTA
+  // valid output window of this tile
   const int OX0 = max(cx0 + H, 0), OX1 = min(cx0 + H + a.tile_x, a.p);
   const int OY0 = max(cy0 + H, 0), OY1 = min(cy0 + H + a.tile_y, a.p);
-
-  int lo[S + 1], hi[S + 1];
-#pragma unroll
-  for (int u = 0; u <= S; ++u) {
-    lo[u] = max(OZ0 - R * (S - u), sz0);
-    hi[u] = min(OZ1 + R * (S - u), sz1);
-  }
 
   // per-cell masks over the thread's VY x V cells (bit j*V+k)
   unsigned ringmask = 0, smask = 0, inmask = 0;
@@ -97,13 +95,15 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
     for (int k = 0; k < V; ++k) {
       const int x = xt + k, y = yt + j;
       const unsigned bit = 1u << (j * V + k);
-      if (x < a.i0 || x >= a.i1 || y < a.i0 || y >= a.i1) ringmask |= bit;
+      if (x >= 0 && x < a.p && y >= 0 && y < a.p) {
+        inmask |= bit;
+        if (x < a.i0 || x >= a.i1 || y < a.i0 || y >= a.i1) ringmask |= bit;
+      }
       if (x >= OX0 && x < OX1 && y >= OY0 && y < OY1) smask |= bit;
-      if (x >= 0 && x < a.p && y >= 0 && y < a.p) inmask |= bit;
     }
-
-  for (int i = tid; i < 2 * S * (NW + 2) * 2 * R * 32 * V; i += NT)
-    (&yedge[0][0][0][0][0][0])[i] = T(0);
+  // every cell of the tile inside the padded grid: loads need no per-element
+  // range checks (CTA-uniform)
+  const bool xy_inside = cx0 >= 0 && cx0 + 32 * V <= a.p && cy0 >= 0 && cy0 + NW * VY <= a.p;
 
   T cur[S][VY][V];
   T acc[S][E][VY][V];
@@ -114,47 +114,54 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
 #pragma unroll
       for (int k = 0; k < V; ++k) cur[u][j][k] = T(0);
 
-  auto issue = [&](int plane) SO2DR_INLINE {
-    const bool ok = plane < hi0;
-    const T* src = a.in + (int64_t)(plane - sz0) * a.plane_stride;
-#pragma unroll
-    for (int j = 0; j < VY; ++j) {
-      const int y = yt + j;
-      const bool rok = ok && y >= 0 && y < a.p;
-#pragma unroll
-      for (int v = 0; v < V; v += VEC)
-        if (rok)
-          issue_vec<T, VEC>(&ring[plane & (RING - 1)][j][tid * V + v], src + (int64_t)y * a.pitch + xt + v,
-                            a.cpb, xt + v, a.pitch);
-    }
-    cp_async_commit();
-  };
-#pragma unroll
-  for (int d = 0; d < RING - 1; ++d) issue(lo0 + d);
-  __syncthreads();
-
-  // steady-state addressing off a running plane offset (poff = (row0 - sz0) *
-  // plane_stride, advanced once per iteration): load plane row0 + RING - 1,
-  // store plane row0 - S(R+1); the thread's (y, x) part is loop-invariant
+  // running plane offset: poff = (lo0 + it - sz0) * plane_stride; loads plane
+  // lo0 + it + RING - 1, stores plane lo0 + it - S(R+1); the thread's (y, x)
+  // part is loop-invariant
   int64_t poff = (int64_t)(lo0 - sz0) * a.plane_stride;
-  const T* ld_thr = a.in + (int64_t)(RING - 1) * a.plane_stride + (int64_t)yt * a.pitch + xt;
-  T* st_thr = a.out - (int64_t)(S * (R + 1)) * a.plane_stride + (int64_t)yt * a.pitch + xt;
-  auto issue_fast = [&](int plane) SO2DR_INLINE {
+  const int64_t yx = (int64_t)yt * a.pitch + xt;
+  const T* ld_thr = a.in + (int64_t)(RING - 1) * a.plane_stride + yx;
+  T* st_thr = a.out - (int64_t)(S * (R + 1)) * a.plane_stride + yx;
+  auto issue = [&](int plane, int64_t off) SO2DR_INLINE {
     if (plane < hi0) {
 #pragma unroll
-      for (int j = 0; j < VY; ++j)
-        issue_inrow<V * (int)sizeof(T)>(&ring[plane & (RING - 1)][j][tid * V], ld_thr + poff + (int64_t)j * a.pitch);
+      for (int j = 0; j < VY; ++j) {
+        if (!xy_inside) {
+          const int y = yt + j;
+          if (y >= 0 && y < a.p) {
+            const T* src = a.in + (int64_t)(plane - sz0) * a.plane_stride + (int64_t)y * a.pitch;
+#pragma unroll
+            for (int v = 0; v < V; v += (V * (int)sizeof(T) >= 16 ? 16 / (int)sizeof(T) : V)) {
+              constexpr int VEC = (V * (int)sizeof(T) >= 16) ? 16 / (int)sizeof(T) : V;
+              issue_vec<T, VEC>(&ring[plane & (RING - 1)][j][tid * V + v], src + xt + v, a.cpb, xt + v, a.pitch);
+            }
+          }
+        } else {
+          issue_inrow<V * (int)sizeof(T)>(&ring[plane & (RING - 1)][j][tid * V], ld_thr + off + (int64_t)j * a.pitch);
+        }
+      }
     }
     cp_async_commit();
   };
+#pragma unroll
+  for (int d = 0; d < RING - 1; ++d) issue(lo0 + d, (int64_t)(d - (RING - 1)) * a.plane_stride + poff);
 
-  auto passthru = [&](int plane, int j, int k) SO2DR_INLINE -> T {
-    const int x = xt + k, y = yt + j;
-    if (x < 0 || x >= a.p || y < 0 || y >= a.p) return T(0);
-    return __ldg(a.in + (int64_t)(plane - sz0) * a.plane_stride + (int64_t)y * a.pitch + x);
+  // CTA-uniform: does this item own any pass-through cell (ring column/row of
+  // the tile, or a ring plane in the z range its stages emit)?
+  const bool tile_edge = __syncthreads_or(ringmask != 0) || lo0 - H < a.iz0 || OZ1 + H > a.iz1;
+  auto passthru = [&](int plane, T (&v)[VY][V]) SO2DR_INLINE {
+    if (plane < sz0 || plane >= sz1) return;
+    const bool ring_plane = plane < a.iz0 || plane >= a.iz1;
+    const unsigned m = ring_plane ? inmask : ringmask;
+    if (!m) return;
+    const T* g = a.in + (int64_t)(plane - sz0) * a.plane_stride + yx;
+#pragma unroll
+    for (int j = 0; j < VY; ++j)
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+        if (m & (1u << (j * V + k))) v[j][k] = __ldg(g + (int64_t)j * a.pitch + k);
   };
 
-  auto publish_edges = [&](int par, int u, const T (&v)[VY][V]) {
+  auto publish_edges = [&](int par, int u, const T (&v)[VY][V]) SO2DR_INLINE {
 #pragma unroll
     for (int j = 0; j < R; ++j)
 #pragma unroll
@@ -164,20 +171,15 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
       }
   };
 
-  // FAST = steady state of a CTA whose whole tile is interior: every stage
-  // consumes and emits interior planes, no ring pass-through, no grid-edge
-  // masking -- all range checks compile away (as in the 2D K1).
-  auto body = [&](auto phase_tag, auto fast_tag, int it) SO2DR_INLINE {
-    constexpr int PH = decltype(phase_tag)::value;
-    constexpr bool FAST = decltype(fast_tag)::value;
-    const int par = it & 1, ppar = par ^ 1;
+  // unrolled by 2E: the accumulator slot (it mod E) and the edge-exchange
+  // parity (it mod 2) are compile-time in every phase
+  auto body = [&](auto phase_tag, int it) SO2DR_INLINE {
+    constexpr int PH = decltype(phase_tag)::value % E;
+    constexpr int par = decltype(phase_tag)::value & 1, ppar = par ^ 1;
     const int row0 = lo0 + it;
 #pragma unroll
     for (int u = S; u >= 1; --u) {
-      const int A = row0 - u - (u - 1) * R;
-      const int Ez = A - R;
-      const bool consume = FAST || (A >= lo[u - 1] && A < hi[u - 1]);
-      const bool emit = FAST || (Ez >= lo[u] && Ez < hi[u]);
+      const int Ez = row0 - u - (u - 1) * R - R;  // plane emitted by stage u
 
       // neighbourhood of the consumed plane: rows yt-R .. yt+VY-1+R,
       // cols xt-R .. xt+V-1+R
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
       for (int j = 0; j < R; ++j)
 #pragma unroll
         for (int k = 0; k < V; ++k) {
-          nb[j][R + k] = yedge[ppar][u - 1][warp][1][j][lane * V + k];          // warp above, bottom rows
+          nb[j][R + k] = yedge[ppar][u - 1][warp][1][j][lane * V + k];              // warp above, bottom rows
           nb[R + VY + j][R + k] = yedge[ppar][u - 1][warp + 2][0][j][lane * V + k];  // warp below, top rows
         }
 #pragma unroll
@@ -201,165 +203,141 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
           nb[j][R + V + q] = __shfl_down_sync(0xffffffffu, nb[j][R + q], 1);
         }
 
-      if (consume) {
 #pragma unroll
-        for (int m = 0; m < E; ++m) {
-          const int dz = m - R;
-          const int sl = (PH - m + 2 * E) % E;
-#pragma unroll
-          for (int j = 0; j < VY; ++j)
-#pragma unroll
-            for (int k = 0; k < V; ++k) {
-              T x = (m == 0) ? T(0) : acc[u - 1][sl][j][k];
-              if constexpr (KIND == KBOX) {
-#pragma unroll
-                for (int dy = -R; dy <= R; ++dy)
-#pragma unroll
-                  for (int dx = -R; dx <= R; ++dx)
-                    x = fma_rn(a.w[((dz + R) * E + dy + R) * E + dx + R], nb[R + j + dy][R + k + dx], x);
-              } else if (dz != 0) {
-                x = fma_rn(a.w[((dz + R) * E + R) * E + R], nb[R + j][R + k], x);
-              } else {
-#pragma unroll
-                for (int dy = -R; dy < 0; ++dy)
-                  x = fma_rn(a.w[(R * E + dy + R) * E + R], nb[R + j + dy][R + k], x);
-#pragma unroll
-                for (int dx = -R; dx <= R; ++dx)
-                  x = fma_rn(a.w[(R * E + R) * E + dx + R], nb[R + j][R + k + dx], x);
-#pragma unroll
-                for (int dy = 1; dy <= R; ++dy)
-                  x = fma_rn(a.w[(R * E + dy + R) * E + R], nb[R + j + dy][R + k], x);
-              }
-              acc[u - 1][sl][j][k] = x;
-            }
-        }
-      }
-
-      if (emit) {
-        constexpr int se = (PH - 2 * R + 2 * E) % E;
-        T outv[VY][V];
-        const bool ring_plane = !FAST && (Ez < a.iz0 || Ez >= a.iz1);
+      for (int m = 0; m < E; ++m) {
+        const int dz = m - R;
+        const int sl = (PH - m + 2 * E) % E;
 #pragma unroll
         for (int j = 0; j < VY; ++j)
 #pragma unroll
           for (int k = 0; k < V; ++k) {
-            outv[j][k] = acc[u - 1][se][j][k];
-            if constexpr (!FAST)
-              if (ring_plane || (ringmask & (1u << (j * V + k)))) outv[j][k] = passthru(Ez, j, k);
+            T x = (m == 0) ? T(0) : acc[u - 1][sl][j][k];
+            if constexpr (KIND == KBOX) {
+#pragma unroll
+              for (int dy = -R; dy <= R; ++dy)
+#pragma unroll
+                for (int dx = -R; dx <= R; ++dx)
+                  x = fma_rn(a.w[((dz + R) * E + dy + R) * E + dx + R], nb[R + j + dy][R + k + dx], x);
+            } else if (dz != 0) {
+              x = fma_rn(a.w[((dz + R) * E + R) * E + R], nb[R + j][R + k], x);
+            } else {
+#pragma unroll
+              for (int dy = -R; dy < 0; ++dy)
+                x = fma_rn(a.w[(R * E + dy + R) * E + R], nb[R + j + dy][R + k], x);
+#pragma unroll
+              for (int dx = -R; dx <= R; ++dx)
+                x = fma_rn(a.w[(R * E + R) * E + dx + R], nb[R + j][R + k + dx], x);
+#pragma unroll
+              for (int dy = 1; dy <= R; ++dy)
+                x = fma_rn(a.w[(R * E + dy + R) * E + R], nb[R + j + dy][R + k], x);
+            }
+            acc[u - 1][sl][j][k] = x;
           }
-        if (u == S) {
-          if constexpr (FAST) {
-            T* dst = st_thr + poff;
+      }
+
+      constexpr int se = (PH - 2 * R + 2 * E) % E;
+      T outv[VY][V];
 #pragma unroll
-            for (int j = 0; j < VY; ++j)
+      for (int j = 0; j < VY; ++j)
 #pragma unroll
-              for (int k = 0; k < V; ++k)
-                if (smask & (1u << (j * V + k))) dst[(int64_t)j * a.pitch + k] = outv[j][k];
-          } else {
-            T* dst = a.out + (int64_t)(Ez - sz0) * a.plane_stride;
-#pragma unroll
-            for (int j = 0; j < VY; ++j)
-#pragma unroll
-              for (int k = 0; k < V; ++k)
-                if (smask & (1u << (j * V + k))) dst[(int64_t)(yt + j) * a.pitch + xt + k] = outv[j][k];
-          }
-        } else {
+        for (int k = 0; k < V; ++k) outv[j][k] = acc[u - 1][se][j][k];
+      if (tile_edge) passthru(Ez, outv);
+      if (u == S) {
+        if (Ez >= OZ0 && Ez < OZ1) {
+          T* dst = st_thr + poff;
 #pragma unroll
           for (int j = 0; j < VY; ++j)
 #pragma unroll
-            for (int k = 0; k < V; ++k) cur[u][j][k] = outv[j][k];
-          publish_edges(par, u, outv);
+            for (int k = 0; k < V; ++k)
+              if (smask & (1u << (j * V + k))) dst[(int64_t)j * a.pitch + k] = outv[j][k];
         }
+      } else {
+#pragma unroll
+        for (int j = 0; j < VY; ++j)
+#pragma unroll
+          for (int k = 0; k < V; ++k) cur[u][j][k] = outv[j][k];
+        publish_edges(par, u, outv);
       }
     }
 
     // stage 0
-    if constexpr (FAST)
-      issue_fast(row0 + RING - 1);
-    else
-      issue(row0 + RING - 1);
+    issue(row0 + RING - 1, poff);
     cp_async_wait<RING - 1>();
-    if (FAST || row0 < hi0) {
 #pragma unroll
-      for (int j = 0; j < VY; ++j)
+    for (int j = 0; j < VY; ++j)
 #pragma unroll
-        for (int k = 0; k < V; ++k)
-          cur[0][j][k] = (FAST || (inmask & (1u << (j * V + k)))) ? ring[row0 & (RING - 1)][j][tid * V + k] : T(0);
-      publish_edges(par, 0, cur[0]);
-    }
+      for (int k = 0; k < V; ++k)
+        cur[0][j][k] = ring[row0 & (RING - 1)][j][tid * V + k];  // (cells off the grid: unread stale values, outside every stored cone)
+    publish_edges(par, 0, cur[0]);
     poff += a.plane_stride;
     __syncthreads();
   };
 
-  // steady-state window [f_lo, f_hi) of iterations (same derivation as 2D);
-  // CTA-uniform, so the one barrier per iteration stays uniform
-  int f_lo = 0, f_hi = hi0 - lo0;
-#pragma unroll
-  for (int u = 1; u <= S; ++u) {
-    const int c = lo0 - u - (u - 1) * R;
-    f_lo = max(f_lo, lo[u - 1] - c);
-    f_hi = min(f_hi, hi[u - 1] - c);
-    f_lo = max(f_lo, max(lo[u], a.iz0) + R - c);
-    f_hi = min(f_hi, min(hi[u], a.iz1) + R - c);
-  }
-  const bool tile_interior = cx0 >= a.i0 && cx0 + 32 * V <= a.i1 && cy0 >= a.i0 && cy0 + NW * VY <= a.i1;
-  if (!tile_interior) f_hi = f_lo;
-
   int it = 0;
-  auto run_general = [&](int stop) SO2DR_INLINE {
-    while (it < stop) {
-      [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
-        ((it < stop ? (body(std::integral_constant<int, Ps>{}, std::false_type{}, it), ++it, void()) : void()),
-         ...);
-      }(std::make_integer_sequence<int, E>{});
-    }
-  };
-  // (the radius-2 box's 125-tap pipeline has no register room for a second
-  // copy of the loop: it runs the general path only, no spill)
-  if constexpr (!(KIND == KBOX && R >= 2)) {
-    const int fl = (f_lo + E - 1) / E * E;
-    if (f_hi - fl >= E) {
-      run_general(fl);
-      while (it + E <= f_hi) {
-        [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
-          ((body(std::integral_constant<int, Ps>{}, std::true_type{}, it), ++it), ...);
-        }(std::make_integer_sequence<int, E>{});
-      }
+  while (it < n_iter) {
+    [&]<int... Ps>(std::integer_sequence<int, Ps...>) {
+      ((it < n_iter ? (body(std::integral_constant<int, Ps>{}, it), ++it, void()) : void()), ...);
+    }(std::make_integer_sequence<int, 2 * E>{});
+  }
+  cp_async_wait<0>();
+}
+
+// Persistent CTAs with dynamic tile scheduling (one wave; no partial last
+// wave): every CTA pulls (tile, z segment) items from a per-stream counter and
+// re-arms it at the end (k1_next_counter).
+template <typename T, int R, int S, int KIND, int V, int VY, int NT>
+__global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int NW = NT / 32;
+  __shared__ int s_item;
+  using YEdge = T[2][S][NW + 2][2][R][32 * V];
+  YEdge& yedge = *reinterpret_cast<YEdge*>(smem_raw + sizeof(T[4][VY][NT * V]));
+  // the guard warps' edge rows (above warp 0 / below the last warp) are never
+  // written: zero them once (finite garbage for the tile's outer halo)
+  for (int i = threadIdx.x; i < 2 * S * (NW + 2) * 2 * R * 32 * V; i += NT) (&yedge[0][0][0][0][0][0])[i] = T(0);
+  const int total = a.nx * a.ny * a.nz;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = static_cast<int>(atomicAdd(a.counter, 1u));
+    __syncthreads();
+    const int item = s_item;
+    if (item >= total) break;
+    const int tz = item / (a.nx * a.ny), rem = item - tz * a.nx * a.ny;
+    const int ty = rem / a.nx, tx = rem - ty * a.nx;
+    k1_tile3d<T, R, S, KIND, V, VY, NT>(a, tx, ty, tz, smem_raw);
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.counter + 1, 1u) == gridDim.x - 1) {
+      a.counter[0] = 0u;
+      a.counter[1] = 0u;
+      __threadfence();
     }
   }
-  run_general(n_iter);
-  cp_async_wait<0>();
 }
 
 namespace {
 
 inline int fdiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
-// Tile shape of the 3D K1 per thread (V x VY cells) and CTA size. Default
-// 2x2 cells, 512 threads. SO2DR_K1_3D=42 / 44 select 4x2 / 4x4 cells on 256
-// threads for fp32 radius 1 (experiments: more FMAs per shuffle/LDS/barrier).
-inline int k1_3d_shape() {
-  static int v = [] {
-    const char* e = std::getenv("SO2DR_K1_3D");
-    return e ? std::atoi(e) : 22;
-  }();
-  return v;
-}
-
-template <typename T, int R, int S, int KIND, int V = 2, int VY = 2,
-          int NT = (sizeof(T) == 8 && R == 2) ? 256 : 512>
+template <typename T, int R, int S, int KIND, int V = 2, int VY = 4, int NT = 256>
 cudaError_t launch3(const K1Launch& L, cudaStream_t stream) {
-  // 512 threads cap registers at 128; the fp64 radius-2 box needs more (a spill
-  // otherwise), so it runs 256-thread CTAs
+  // 2x4 cells per thread on 256 threads: the same 64x32 tile as 2x2 on 512,
+  // fewer shuffles / edge rows per cell, and room (255 registers) for both
+  // the inner and the edge variant of the pipeline without spills
   constexpr int NW = NT / 32, H = R * S;
   constexpr size_t smem = sizeof(T) * (4 * VY * NT * V + 2 * S * (NW + 2) * 2 * R * 32 * V);
   static_assert(smem <= 227 * 1024, "3D K1 shared memory");
   auto kern = k1_stencil3d<T, R, S, KIND, V, VY, NT>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
+  static bool attr_done[64] = {};
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr_done[dev]) {  // per device: the attribute applies to the current device only
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_done[dev] = true;
+    }
   }
   constexpr int CPB = (V * (int)sizeof(T)) >= 16 ? 16 : V * (int)sizeof(T);
   constexpr int VEC = CPB / (int)sizeof(T);
@@ -394,12 +372,25 @@ cudaError_t launch3(const K1Launch& L, cudaStream_t stream) {
   const int depth = L.y1 - L.y0;
   const int sms = device_sm_count();
   const int min_seg = std::max(16, 4 * (H + S * (R + 1)));
-  int nz = std::max(1, (4 * sms + nx * ny - 1) / (nx * ny));
+  int nz = std::max(1, (8 * sms + nx * ny - 1) / (nx * ny));
   nz = std::min(nz, std::max(1, depth / min_seg));
   a.seg = (depth + nz - 1) / nz;
   nz = (depth + a.seg - 1) / a.seg;
-  dim3 grid(nx, ny, nz);
-  kern<<<grid, NT, smem, stream>>>(a);
+  a.nx = nx;
+  a.ny = ny;
+  a.nz = nz;
+  a.counter = k1_next_counter(stream);
+  if (!a.counter) return cudaErrorUnknown;
+  static int occ_by_dev[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  int occ = occ_by_dev[dev];
+  if (occ == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem) != cudaSuccess || occ < 1) occ = 1;
+    occ_by_dev[dev] = occ;
+  }
+  const int ctas = std::max(1, std::min(sms * occ, nx * ny * nz));
+  kern<<<ctas, NT, smem, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -414,13 +405,11 @@ cudaError_t launch3_s(const K1Launch& L, cudaStream_t stream) {
     return cudaErrorInvalidValue;
   } else {
     if (L.steps == S) {
-      if constexpr (sizeof(T) == 4 && R == 1) {
-        if (k1_3d_shape() == 42) return launch3<T, R, S, KIND, 4, 2, 256>(L, stream);
-        if constexpr (S <= 2) {
-          if (k1_3d_shape() == 44) return launch3<T, R, S, KIND, 4, 4, 256>(L, stream);
-        }
-      }
-      return launch3<T, R, S, KIND>(L, stream);
+      // radius 2 box (125 taps) and fp64 radius 2: 2x2 cells per thread (the
+      // 2x4 pipeline spills)
+      if constexpr (R == 2 && (KIND == KBOX || sizeof(T) == 8)) return launch3<T, R, S, KIND, 2, 2, 256>(L, stream);
+      else if constexpr (sizeof(T) == 4 && R == 1 && SO2DR_K3D_SHAPE == 22) return launch3<T, R, S, KIND, 2, 2, 512>(L, stream);
+      else return launch3<T, R, S, KIND>(L, stream);
     }
     return launch3_s<T, R, KIND, S + 1>(L, stream);
   }

@@ -96,3 +96,24 @@ def test_2d_f64_engine(engine, oracle, kind, r):
     assert (_bits(got) == _bits(want)).all()
     # the stated fp64 tolerance (<= 1e-12 relative) holds trivially: bit-exact
     assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["f32", "f64"])
+@pytest.mark.parametrize("kind,r", [("star", 1), ("box", 1), ("rand", 1), ("star", 2), ("box", 2)])
+def test_3d_inner_tiles_every_depth(engine, oracle, dtype, kind, r):
+    """Grids wide enough for inner tiles (the check-free streaming body) next to
+    edge tiles, every fused depth the 3D K1 supports, out-of-core chunks with
+    region sharing (so2dr) and in-core."""
+    sz = 136 if r == 1 else 104
+    spec, okind, w = _spec3(kind, r, dtype)
+    g = oracle.init_grid(sz, r, 21 + r, 3, dtype)
+    kmax = so2dr.k1_max_steps(3, dtype, so2dr.BOX if kind != "star" else so2dr.STAR, r)
+    for k_on in range(1, kmax + 1):
+        n = 2 * k_on
+        for mode, d in (("incore", 1), ("so2dr", 2)):
+            cfg = so2dr.RunConfig(sz=sz, r=r, d=d, s_tb=n, k_on=k_on, n_strm=2, n=n)
+            got = g.copy()
+            engine.run(mode, got, spec, cfg, so2dr.KernelPlan(k_on, 32, 1 << 30))
+            want = oracle.run(g, okind, r, w, n)
+            diff = np.argwhere(_bits(got) != _bits(want))
+            assert diff.size == 0, f"{mode} {kind}{r} {np.dtype(dtype).name} k_on={k_on}: {len(diff)} diffs, first {diff[:3]}"
