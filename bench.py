@@ -57,16 +57,16 @@ def peaks():
         return {}
 
 
-def geometry(world: int):
-    d = D_PER_RANK * world
+def geometry(world: int, d_per_rank: int = D_PER_RANK):
+    d = d_per_rank * world
     sz = SZ1 if world == 1 else int(round(SZ1 * math.sqrt(world) / d)) * d
     return sz, d
 
 
-def workload_desc(world, sz, d):
+def workload_desc(world, sz, d, k_on=K_ON):
     gb = (sz + 2 * R) ** 2 * 4 / 1e9
     return (f"box2d1r fp32 out-of-core, sz={sz} ({gb:.2f} GB grid, {gb / world / (BUDGET / 1e9):.2f}x the "
-            f"{BUDGET >> 30} GiB per-GPU HBM budget), n={NSTEPS} timesteps, d={d}, S_TB={S_TB}, k_on={K_ON}, "
+            f"{BUDGET >> 30} GiB per-GPU HBM budget), n={NSTEPS} timesteps, d={d}, S_TB={S_TB}, k_on={k_on}, "
             f"N_strm={NSTRM}, slab-partitioned over {world} GPU(s)")
 
 
@@ -310,6 +310,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--k-on", type=int, default=K_ON)
+    ap.add_argument("--d", type=int, default=D_PER_RANK, help="chunks per rank")
+    ap.add_argument("--plan", action="store_true",
+                    help="take d and k_on from the B200 planner (include/so2dr/b200.hpp) instead of --d/--k-on")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hbm-leg", "--no-value-leg", dest="no_hbm_leg", action="store_true")
     ap.add_argument("--pcie-probe-before", action="store_true",
@@ -337,7 +340,19 @@ def main():
     dev = torch.device("cuda", dev_index)
 
     k_on = args.k_on
-    sz, d = geometry(world)
+    sz, d = geometry(world, args.d)
+    # B200 planner (profiles/b200.json): its choice for this workload and its
+    # prediction for the configuration actually run
+    try:
+        prof = open(os.path.join(ROOT, "profiles", "b200.json")).read()
+    except OSError:
+        prof = None
+    pick = so2dr.plan_b200(sz, NSTEPS, R, so2dr.BOX, budget_bytes=BUDGET, n_strm=NSTRM, profile=prof)
+    if args.plan:
+        k_on = pick["k_on"]
+        sz, d = geometry(world, pick["d"])
+    pred = so2dr.predict_b200(sz, NSTEPS, d // world, S_TB, k_on, R, so2dr.BOX, budget_bytes=BUDGET,
+                              n_strm=NSTRM, profile=prof) if world == 1 else None
     cfg = so2dr.RunConfig(sz=sz, r=R, d=d, s_tb=S_TB, k_on=k_on, n_strm=NSTRM, n=NSTEPS)
     spec = so2dr.StencilSpec.box(R)
     kp = so2dr.KernelPlan(k_on, 32, 64 << 20)
@@ -465,7 +480,7 @@ def main():
         "ms_per_step": e2e_res["device_ms_total"] / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (splitmix64 init_grid, seed 42; grid generated on device)",
-        "config": {"workload": workload_desc(world, sz, d), "sz": sz, "d": d, "s_tb": S_TB, "k_on": k_on,
+        "config": {"workload": workload_desc(world, sz, d, k_on), "sz": sz, "d": d, "s_tb": S_TB, "k_on": k_on,
                    "n": NSTEPS, "n_strm": NSTRM, "budget_bytes_per_gpu": BUDGET,
                    "grid_bytes": (sz + 2 * R) ** 2 * 4,
                    "l2": "no flush needed: every step streams the whole grid (>= 34 GB >> 126 MB L2)",
@@ -498,6 +513,12 @@ def main():
                                  "d2h": e2e_res["d2h"] / (e2e_res["device_ms_total"] / 1e3) / 1e9,
                                  "note": "ledger bytes / e2e device time (includes pipeline fill and drain)"},
                              "formula": "R_pcie = G*BW_pcie_dir(duplex)*S_TB/b ; R_hbm = G*BW_hbm/(2b/k_on + 2b/S_TB)"},
+        "planner": {"choice": {k: pick[k] for k in ("d", "s_tb", "k_on", "n_strm", "t_total_s", "gcell_per_s")},
+                    "predicted_for_this_config": ({k: pred[k] for k in ("t_total_s", "t_pcie_s", "t_kernel_s",
+                                                                          "t_fill_s", "gcell_per_s")}
+                                                  if pred else None),
+                    "source": "so2dr_plan_b200 over (d | sz, S_TB | n, k_on <= 8), profiles/b200.json",
+                    "used": bool(args.plan)},
         "cpu_baseline": cb,
         "clocks": clocks,
         "gpu_launches": e2e_res["launches"],

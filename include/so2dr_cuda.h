@@ -248,6 +248,30 @@ so2dr_status so2dr_expected_ledger(so2dr_mode mode, const so2dr_run_config* cfg,
                                    const so2dr_kernel_plan* kp, int dim, so2dr_dtype dtype,
                                    uint64_t out6[6], int32_t* exact);
 
+/* ---- B200 run planner (host-only) ---------------------------
+ * Replaces the reference's predict_bottleneck / feasible_configs model
+ * (proj/src/planner.cpp:14-89: t_kernel = S_TB one-step sweeps, one buffer per
+ * stream) with the engine's pipeline: k_on-fused K1 launches priced from a
+ * measured profile (profiles/b200.json; NULL = the built-in copy), the duplex
+ * PCIe rate, pipeline fill/drain and the real device footprint
+ * (include/so2dr/b200.hpp). `star` = star taps, else box. */
+typedef struct {
+  int32_t d, s_tb, k_on, n_strm, feasible;
+  int64_t launches;
+  uint64_t device_bytes;
+  double t_pcie_s, t_kernel_s, t_fill_s, t_total_s, gcell_per_s;
+} so2dr_plan_entry;
+/* Every (d | sz, S_TB | n, k_on <= min(S_TB, 8)) candidate at n_strm streams
+ * (up to `capacity` written to entries, *count = total) and the fastest
+ * feasible one in *best. */
+so2dr_status so2dr_plan_b200(const char* profile_json, int dim, so2dr_dtype dtype, int star, int radius,
+                             int sz, int n, uint64_t budget_bytes, int n_strm, so2dr_plan_entry* best,
+                             so2dr_plan_entry* entries, int32_t capacity, int32_t* count);
+/* The prediction for one configuration. */
+so2dr_status so2dr_predict_b200(const char* profile_json, int dim, so2dr_dtype dtype, int star, int radius,
+                                int sz, int n, uint64_t budget_bytes, int d, int s_tb, int k_on,
+                                int n_strm, so2dr_plan_entry* out);
+
 /* ---- spec files, presets and run outputs (host-only) ----------------------
  * RunSpecFile / parse_spec_json / parse_spec_file  proj/include/so2dr/specfile.hpp:14-28
  * presets (--preset NAME)                          proj/tools/so2dr_main.cpp:28-68

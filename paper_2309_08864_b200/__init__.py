@@ -11,6 +11,7 @@ without the built library or a CUDA device the calls raise.
 from __future__ import annotations
 
 import ctypes
+import json
 import dataclasses
 import os
 from typing import Optional, Sequence
@@ -128,6 +129,7 @@ EXPORTS = (
     "so2dr_slab_rows", "so2dr_slab_prepare", "so2dr_slab_connect", "so2dr_slab_run",
     "so2dr_fused_kernel", "so2dr_apply_step", "so2dr_run_reference", "so2dr_init_grid",
     "so2dr_init_rows", "so2dr_grid_checksum", "so2dr_arena_bytes", "so2dr_device_bytes", "so2dr_k1_max_steps",
+    "so2dr_plan_b200", "so2dr_predict_b200",
     "so2dr_plan_chunks", "so2dr_expected_ledger", "so2dr_kernel_stats",
     "so2dr_spec_parse", "so2dr_spec_parse_file", "so2dr_preset_count", "so2dr_preset_name",
     "so2dr_preset_json", "so2dr_report_json", "so2dr_ledger_csv", "so2dr_diagnostics_csv",
@@ -606,6 +608,50 @@ def arena_bytes(config: RunConfig, kernel: KernelPlan) -> int:
     out = ctypes.c_uint64()
     _check(lib().so2dr_arena_bytes(ctypes.byref(config._c()), ctypes.byref(kernel._c()), ctypes.byref(out)))
     return out.value
+
+
+class _PlanEntry(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("s_tb", ctypes.c_int32), ("k_on", ctypes.c_int32),
+                ("n_strm", ctypes.c_int32), ("feasible", ctypes.c_int32), ("launches", ctypes.c_int64),
+                ("device_bytes", ctypes.c_uint64), ("t_pcie_s", ctypes.c_double), ("t_kernel_s", ctypes.c_double),
+                ("t_fill_s", ctypes.c_double), ("t_total_s", ctypes.c_double), ("gcell_per_s", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def _plan_args(profile, dim, dtype, kind, radius):
+    prof = None if profile is None else (profile if isinstance(profile, str) else json.dumps(profile)).encode()
+    code = 0 if np.dtype(dtype) == np.float32 else 1
+    return prof, dim, code, 1 if kind == STAR else 0, radius
+
+
+def plan_b200(sz: int, n: int, radius: int = 1, kind: int = BOX, dim: int = 2, dtype=np.float32,
+              budget_bytes: int = 0, n_strm: int = 3, profile=None, all_candidates: bool = False):
+    """B200 planner (include/so2dr/b200.hpp): the fastest feasible (d, S_TB, k_on)
+    for an so2dr run, priced from profiles/b200.json (profile=None: built-in copy;
+    a JSON string or dict overrides)."""
+    prof, dim, code, star, radius = _plan_args(profile, dim, dtype, kind, radius)
+    best = _PlanEntry()
+    count = ctypes.c_int32()
+    _check(lib().so2dr_plan_b200(prof, dim, code, star, radius, sz, n, ctypes.c_uint64(budget_bytes), n_strm,
+                                 ctypes.byref(best), None, 0, ctypes.byref(count)))
+    if not all_candidates:
+        return best.as_dict()
+    arr = (_PlanEntry * count.value)()
+    _check(lib().so2dr_plan_b200(prof, dim, code, star, radius, sz, n, ctypes.c_uint64(budget_bytes), n_strm,
+                                 ctypes.byref(best), arr, count.value, ctypes.byref(count)))
+    return best.as_dict(), [e.as_dict() for e in arr]
+
+
+def predict_b200(sz: int, n: int, d: int, s_tb: int, k_on: int, radius: int = 1, kind: int = BOX, dim: int = 2,
+                 dtype=np.float32, budget_bytes: int = 0, n_strm: int = 3, profile=None) -> dict:
+    """The B200 planner's prediction for one configuration."""
+    prof, dim, code, star, radius = _plan_args(profile, dim, dtype, kind, radius)
+    out = _PlanEntry()
+    _check(lib().so2dr_predict_b200(prof, dim, code, star, radius, sz, n, ctypes.c_uint64(budget_bytes), d, s_tb,
+                                    k_on, n_strm, ctypes.byref(out)))
+    return out.as_dict()
 
 
 def k1_max_steps(dim: int, dtype, kind: int, radius: int) -> int:

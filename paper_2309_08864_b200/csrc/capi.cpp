@@ -2,6 +2,7 @@
 // structs into engine requests and the library's exception types
 // (include/so2dr/errors.hpp, mirroring proj/include/so2dr/errors.hpp) into
 // so2dr_status codes plus a per-context message.
+#include <algorithm>
 #include <cstdlib>
 #include <cuda_runtime.h>
 
@@ -10,6 +11,7 @@
 
 #include "engine.h"
 #include "k1_launch.h"
+#include "so2dr/b200.hpp"
 #include "so2dr/report.hpp"
 #include "so2dr/specfile.hpp"
 #include "so2dr/verify.hpp"
@@ -378,6 +380,59 @@ so2dr_status so2dr_arena_bytes(const so2dr_run_config* cfg, const so2dr_kernel_p
   return guard(nullptr, [&] {
     if (!out) throw so2dr::ContractError("arena_bytes: out is NULL");
     *out = so2dr::so2dr_arena_bytes(to_cfg(cfg), to_kp(kp));
+  });
+}
+
+namespace {
+so2dr::b200::Profile plan_profile(const char* json) {
+  return json ? so2dr::b200::profile_from_json(json, "<argument>") : so2dr::b200::default_profile();
+}
+so2dr::b200::Problem plan_problem(int dim, so2dr_dtype dtype, int star, int radius, int sz, int n,
+                                  uint64_t budget, int n_strm) {
+  so2dr::b200::Problem pb;
+  if (dim != 2 && dim != 3) throw so2dr::ContractError("planner: dim must be 2 or 3");
+  pb.dim = dim;
+  pb.elem_bytes = dtype == SO2DR_F64 ? 8 : 4;
+  pb.star = star != 0;
+  pb.radius = radius;
+  pb.sz = sz;
+  pb.n = n;
+  pb.budget = budget;
+  pb.n_strm = {n_strm};
+  return pb;
+}
+void to_entry(const so2dr::b200::Candidate& c, so2dr_plan_entry* e) {
+  e->d = c.d, e->s_tb = c.s_tb, e->k_on = c.k_on, e->n_strm = c.n_strm, e->feasible = c.feasible;
+  e->launches = c.launches;
+  e->device_bytes = c.device_bytes;
+  e->t_pcie_s = c.t_pcie, e->t_kernel_s = c.t_kernel, e->t_fill_s = c.t_fill, e->t_total_s = c.t_total;
+  e->gcell_per_s = c.gcells;
+}
+}  // namespace
+
+so2dr_status so2dr_plan_b200(const char* profile_json, int dim, so2dr_dtype dtype, int star, int radius,
+                             int sz, int n, uint64_t budget_bytes, int n_strm, so2dr_plan_entry* best,
+                             so2dr_plan_entry* entries, int32_t capacity, int32_t* count) {
+  return guard(nullptr, [&] {
+    if (!best) throw so2dr::ContractError("plan_b200: best is NULL");
+    const auto pl = so2dr::b200::plan(plan_profile(profile_json),
+                                      plan_problem(dim, dtype, star, radius, sz, n, budget_bytes, n_strm));
+    to_entry(pl.best, best);
+    const int32_t total = static_cast<int32_t>(pl.candidates.size());
+    if (count) *count = total;
+    for (int32_t i = 0; entries && i < std::min(capacity, total); ++i) to_entry(pl.candidates[i], &entries[i]);
+  });
+}
+
+so2dr_status so2dr_predict_b200(const char* profile_json, int dim, so2dr_dtype dtype, int star, int radius,
+                                int sz, int n, uint64_t budget_bytes, int d, int s_tb, int k_on,
+                                int n_strm, so2dr_plan_entry* out) {
+  return guard(nullptr, [&] {
+    if (!out) throw so2dr::ContractError("predict_b200: out is NULL");
+    const auto c = so2dr::b200::predict(plan_profile(profile_json),
+                                        plan_problem(dim, dtype, star, radius, sz, n, budget_bytes, n_strm), d,
+                                        s_tb, k_on, n_strm);
+    to_entry(c, out);
   });
 }
 

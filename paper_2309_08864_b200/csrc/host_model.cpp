@@ -12,6 +12,7 @@
 
 #include "so2dr/engine.hpp"
 #include "so2dr/gridio.hpp"
+#include "json_lite.hpp"
 #include "so2dr/planner.hpp"
 #include "so2dr/verify.hpp"
 
@@ -587,91 +588,27 @@ std::uint64_t analytic_redundancy(const RunConfig& config) {
   return analytic_redundancy(config, config.s_tb);
 }
 
-// Minimal reader for the flat hardware-profile object
-// {"name": str, "c_dmem_bytes": int, "bw_dmem_bytes_per_s": num,
-//  "bw_intc_bytes_per_s": num, "b_elem": int} (proj/src/planner.cpp:115-143).
-namespace {
-struct FlatJson {
-  std::map<std::string, std::string> strings;
-  std::map<std::string, double> numbers;
-  std::map<std::string, std::uint64_t> integers;
-};
-
-FlatJson parse_flat_object(const std::string& text, const std::string& origin) {
-  FlatJson out;
-  std::size_t i = 0;
-  auto fail = [&](const std::string& why) {
-    throw IoError("hardware profile " + origin + ": " + why + " at offset " + std::to_string(i));
-  };
-  auto ws = [&] {
-    while (i < text.size() && std::isspace(static_cast<unsigned char>(text[i]))) ++i;
-  };
-  auto str = [&]() -> std::string {
-    if (i >= text.size() || text[i] != '"') fail("expected string");
-    std::string s;
-    for (++i; i < text.size() && text[i] != '"'; ++i) {
-      if (text[i] == '\\' && i + 1 < text.size()) ++i;
-      s.push_back(text[i]);
-    }
-    if (i >= text.size()) fail("unterminated string");
-    ++i;
-    return s;
-  };
-  ws();
-  if (i >= text.size() || text[i] != '{') fail("expected '{'");
-  ++i;
-  ws();
-  if (i < text.size() && text[i] == '}') return out;
-  for (;;) {
-    ws();
-    const std::string key = str();
-    ws();
-    if (i >= text.size() || text[i] != ':') fail("expected ':'");
-    ++i;
-    ws();
-    if (i < text.size() && text[i] == '"') {
-      out.strings[key] = str();
-    } else {
-      const std::size_t start = i;
-      while (i < text.size() && (std::isdigit(static_cast<unsigned char>(text[i])) ||
-                                 std::strchr("+-.eE", text[i])))
-        ++i;
-      if (i == start) fail("expected value");
-      const std::string num = text.substr(start, i - start);
-      out.numbers[key] = std::stod(num);
-      if (num.find_first_of(".eE-") == std::string::npos)
-        out.integers[key] = std::stoull(num);
-    }
-    ws();
-    if (i < text.size() && text[i] == ',') {
-      ++i;
-      continue;
-    }
-    if (i < text.size() && text[i] == '}') break;
-    fail("expected ',' or '}'");
-  }
-  return out;
-}
-}  // namespace
-
+// Hardware profile {"name": str, "c_dmem_bytes": int, "bw_dmem_bytes_per_s":
+// num, "bw_intc_bytes_per_s": num, "b_elem": int} (proj/src/planner.cpp:115-143);
+// other keys (profiles/b200.json carries the B200 planner's) are ignored, as
+// the reference's nlohmann reader does.
 HardwareModel hardware_profile_from_json(const std::string& text, const std::string& origin) {
-  const FlatJson j = parse_flat_object(text, origin);
-  auto need_num = [&](const char* k) {
-    const auto it = j.numbers.find(k);
-    if (it == j.numbers.end()) throw IoError("hardware profile " + origin + ": missing " + k);
-    return it->second;
-  };
+  so2dr_json::Value j;
+  try {
+    j = so2dr_json::parse(text);
+  } catch (const so2dr_json::ParseError& e) {
+    throw IoError("hardware profile " + origin + ": " + e.what());
+  }
   HardwareModel hw;
-  const auto nm = j.strings.find("name");
-  hw.name = nm == j.strings.end() ? "unnamed" : nm->second;
-  const auto cd = j.integers.find("c_dmem_bytes");
-  if (cd == j.integers.end())
-    throw IoError("hardware profile " + origin + ": missing integer c_dmem_bytes");
-  hw.c_dmem = cd->second;
-  hw.bw_dmem = need_num("bw_dmem_bytes_per_s");
-  hw.bw_intc = need_num("bw_intc_bytes_per_s");
-  const auto be = j.integers.find("b_elem");
-  hw.b_elem = be == j.integers.end() ? 4 : static_cast<int>(be->second);
+  try {
+    hw.name = j.contains("name") ? j.at("name").as_string() : "unnamed";
+    hw.c_dmem = j.at("c_dmem_bytes").as_uint64();
+    hw.bw_dmem = j.at("bw_dmem_bytes_per_s").as_double();
+    hw.bw_intc = j.at("bw_intc_bytes_per_s").as_double();
+    hw.b_elem = j.contains("b_elem") ? static_cast<int>(j.at("b_elem").as_int64()) : 4;
+  } catch (const std::exception& e) {
+    throw IoError("hardware profile " + origin + ": " + e.what());
+  }
   hw.validate();
   return hw;
 }
