@@ -50,6 +50,27 @@ TAPS = 9  # box2d1r
 BUDGET = 16 << 30
 
 
+def host_numa_nodes() -> int:
+    n = 0
+    while os.path.isdir(f"/sys/devices/system/node/node{n}"):
+        n += 1
+    return n
+
+
+def host_copy_gbps(torch, mib: int = 1024) -> float:
+    """Host DRAM copy bandwidth (read + write bytes), best of 3, all threads."""
+    a = torch.empty(mib << 18, dtype=torch.float32)
+    a.fill_(1.0)
+    b = torch.empty_like(a)
+    best = 0.0
+    for _ in range(3):
+        t0 = time.perf_counter()
+        b.copy_(a)
+        dt = time.perf_counter() - t0
+        best = max(best, 2 * a.numel() * 4 / dt / 1e9)
+    return best
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -407,7 +428,8 @@ def main():
         wall = time.perf_counter() - t0
         dev_ms = allmax(sum(times))
         return {"device_ms_total": dev_ms, "wall_s": allmax(wall), "kernel_ms": kms, "kernel_max_ms": kmax,
-                "launches": launches, "alg_bytes": algb, "h2d": h2d, "d2h": d2h, "per_step_ms": times}
+                "launches": launches, "alg_bytes": algb, "h2d": h2d, "d2h": d2h, "per_step_ms": times,
+                "rank_ms": sum(times)}
 
     total_updates = sz * sz * NSTEPS  # per step, whole job
 
@@ -435,6 +457,14 @@ def main():
     clocks = clk.summary()
     if rank == 0 and not args.pcie_probe_before:
         pc = pcie_probe(torch, dev)
+    # multi-GPU evidence: every rank's own e2e time, its GPU's NUMA node and the
+    # halo transport of its slab edges (all ranks take part in the gather)
+    mine = {"rank": rank, "device_ms": e2e_res["rank_ms"], "numa_node": so2dr.device_numa_node(dev_index),
+            "transport": eng.slab_info() if world > 1 else None}
+    ranks = [mine]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
 
     if rank != 0:
         if world > 1:
@@ -467,6 +497,7 @@ def main():
     r_pcie = world * bw_dir * 1e9 * S_TB / 4 / 1e9
     r_hbm = world * hbm * 1e9 / (2 * 4 / k_on + 2 * 4 / S_TB) / 1e9
     r_bind = min(r_pcie, r_hbm)
+    r_host = host_copy_gbps(torch)
     cb = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -519,6 +550,16 @@ def main():
                                                   if pred else None),
                     "source": "so2dr_plan_b200 over (d | sz, S_TB | n, k_on <= 8), profiles/b200.json",
                     "used": bool(args.plan)},
+        "multi_gpu": {
+            "per_rank": [{"rank": q["rank"], "e2e_GCell_s": total_updates / world * args.steps /
+                          (q["device_ms"] / 1e3) / 1e9, "numa_node": q["numa_node"], "transport": q["transport"]}
+                         for q in ranks],
+            "host_numa_nodes": host_numa_nodes(),
+            "R_host_copy_GBps": r_host,
+            "R_host_note": "host DRAM copy bandwidth (read+write bytes, torch CPU copy, all threads); N ranks "
+                           "stream 2 x BW_pcie_dir each, so host DRAM binds before PCIe once "
+                           "N * 2 * BW_pcie_dir > R_host (SURVEY 7 hard part 7)",
+            "halo_path": "CUDA IPC peer memory + stream memory operations (so2dr_slab_*), no NCCL on the data path"},
         "cpu_baseline": cb,
         "clocks": clocks,
         "gpu_launches": e2e_res["launches"],

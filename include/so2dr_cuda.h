@@ -146,9 +146,18 @@ int so2dr_device_count(void);
 /* Pinned host allocation for grids (cudaHostAlloc, portable). Preferred over
  * registering malloc'd memory: on this pool's B200 hosts, 4 KiB-page
  * registered memory sustains only ~43 GB/s per direction when H2D and D2H
- * overlap, cudaHostAlloc / huge-page memory ~50 GB/s (tools/cu/pin_bench.cu). */
+ * overlap, cudaHostAlloc / huge-page memory ~50 GB/s (tools/cu/pin_bench.cu).
+ * On a multi-socket host the pages are bound to the NUMA node of the
+ * context's GPU (2 MiB-aligned mmap, transparent huge pages, mbind MPOL_BIND,
+ * then cudaHostRegister): each rank's slab streams from its own socket's DRAM
+ * (SURVEY 7 hard part 7). One NUMA node or SO2DR_HOST_NUMA=0: cudaHostAlloc. */
 so2dr_status so2dr_host_alloc(so2dr_ctx* ctx, size_t bytes, void** out);
 so2dr_status so2dr_host_free(so2dr_ctx* ctx, void* p);
+/* NUMA node of a GPU (sysfs numa_node of its PCI function), -1 if unknown. */
+int so2dr_device_numa_node(int device);
+/* NUMA node of the `sysfs_root`/bus/pci/devices/<pci_bus_id>/numa_node file,
+ * -1 if absent (host logic of so2dr_device_numa_node; sysfs_root "" = /sys). */
+int so2dr_pci_numa_node(const char* sysfs_root, const char* pci_bus_id);
 /* Pin a caller-owned host range (cudaHostRegister); idempotent per range. */
 so2dr_status so2dr_host_register(so2dr_ctx* ctx, void* base, size_t bytes);
 so2dr_status so2dr_host_unregister(so2dr_ctx* ctx, void* base);
@@ -187,6 +196,11 @@ so2dr_status so2dr_slab_prepare(so2dr_ctx* ctx, const so2dr_stencil_desc* st,
  * connected by raw pointer (two contexts sharing one process/GPU). */
 so2dr_status so2dr_slab_connect(so2dr_ctx* ctx, const uint8_t* lower_blob,
                                 const uint8_t* upper_blob);
+/* The connected halo transports: out[0] = rank, out[1] = world, out[2] /
+ * out[3] = lower / upper edge: 0 none, 1 same process (raw pointer), 2 CUDA
+ * IPC on the same GPU, 3 CUDA IPC to a peer GPU with peer access confirmed,
+ * 4 CUDA IPC to a GPU this process cannot see (peer access not checkable). */
+so2dr_status so2dr_slab_info(const so2dr_ctx* ctx, int32_t out[4]);
 so2dr_status so2dr_slab_run(so2dr_ctx* ctx, const so2dr_stencil_desc* st,
                             const so2dr_run_config* cfg, const so2dr_kernel_plan* kp,
                             so2dr_dtype dtype, void* slab, so2dr_ledger* ledger_out,

@@ -129,7 +129,7 @@ EXPORTS = (
     "so2dr_slab_rows", "so2dr_slab_prepare", "so2dr_slab_connect", "so2dr_slab_run",
     "so2dr_fused_kernel", "so2dr_apply_step", "so2dr_run_reference", "so2dr_init_grid",
     "so2dr_init_rows", "so2dr_grid_checksum", "so2dr_arena_bytes", "so2dr_device_bytes", "so2dr_k1_max_steps",
-    "so2dr_plan_b200", "so2dr_predict_b200",
+    "so2dr_plan_b200", "so2dr_predict_b200", "so2dr_device_numa_node", "so2dr_pci_numa_node", "so2dr_slab_info",
     "so2dr_plan_chunks", "so2dr_expected_ledger", "so2dr_kernel_stats",
     "so2dr_spec_parse", "so2dr_spec_parse_file", "so2dr_preset_count", "so2dr_preset_name",
     "so2dr_preset_json", "so2dr_report_json", "so2dr_ledger_csv", "so2dr_diagnostics_csv",
@@ -539,6 +539,16 @@ class Engine:
     def slab_connect(self, lower: Optional[bytes], upper: Optional[bytes]):
         self._ck(lib().so2dr_slab_connect(self._h, lower, upper))
 
+    SLAB_TRANSPORTS = {0: "none", 1: "same-process", 2: "ipc-same-gpu", 3: "ipc-peer (p2p checked)",
+                       4: "ipc-peer (not visible here)"}
+
+    def slab_info(self) -> dict:
+        """Rank, world and the halo transport of each slab edge after slab_connect."""
+        out = (ctypes.c_int32 * 4)()
+        self._ck(lib().so2dr_slab_info(self._h, out))
+        return {"rank": out[0], "world": out[1], "lower": self.SLAB_TRANSPORTS[out[2]],
+                "upper": self.SLAB_TRANSPORTS[out[3]]}
+
     def slab_run(self, spec: StencilSpec, config: RunConfig, slab, kernel: Optional[KernelPlan] = None):
         st, keep = spec._c()
         cfg = config._c()
@@ -652,6 +662,16 @@ def predict_b200(sz: int, n: int, d: int, s_tb: int, k_on: int, radius: int = 1,
     _check(lib().so2dr_predict_b200(prof, dim, code, star, radius, sz, n, ctypes.c_uint64(budget_bytes), d, s_tb,
                                     k_on, n_strm, ctypes.byref(out)))
     return out.as_dict()
+
+
+def device_numa_node(device: int = 0) -> int:
+    """NUMA node of a GPU (sysfs), -1 if unknown."""
+    return int(lib().so2dr_device_numa_node(device))
+
+
+def pci_numa_node(pci_bus_id: str, sysfs_root: str = "") -> int:
+    """The sysfs lookup behind device_numa_node (host logic, no GPU needed)."""
+    return int(lib().so2dr_pci_numa_node(sysfs_root.encode(), pci_bus_id.encode()))
 
 
 def k1_max_steps(dim: int, dtype, kind: int, radius: int) -> int:

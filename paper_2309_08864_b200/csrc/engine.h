@@ -80,6 +80,8 @@ Geo make_geo(int dim, int sz, int r, int dtype);
 struct PeerEdge {
   bool connected = false;
   bool ipc = false;
+  bool same_device = false;  // the neighbour context runs on this GPU
+  bool p2p_checked = false;  // cudaDeviceCanAccessPeer confirmed the path
   void* recv = nullptr;        // neighbour's receive buffer for our band (mapped)
   uint32_t* flag = nullptr;    // neighbour's data-ready flag for that buffer
   uint32_t* ack = nullptr;     // neighbour's consumed flag we must wait for (in our memory)

@@ -191,6 +191,7 @@ struct Blob {
   uint64_t off_lo, off_hi, off_flags;
   uint64_t raw;  // base pointer in the owner's address space
   cudaIpcMemHandle_t handle;
+  char pci[32];  // PCI bus id of the owner's GPU (the peer-access check)
 };
 static_assert(sizeof(Blob) <= SO2DR_PEER_BLOB_BYTES, "blob too large");
 }  // namespace
@@ -230,6 +231,7 @@ void slab_prepare(so2dr_ctx* ctx, const StencilDev& st, const so2dr_run_config& 
   b.off_flags = 2 * band_al;
   b.raw = reinterpret_cast<uint64_t>(base);
   SO2DR_CK(cudaIpcGetMemHandle(&b.handle, base));
+  SO2DR_CK(cudaDeviceGetPCIBusId(b.pci, sizeof b.pci, ctx->device));
   std::memset(blob_out, 0, SO2DR_PEER_BLOB_BYTES);
   std::memcpy(blob_out, &b, sizeof(b));
 }
@@ -247,6 +249,25 @@ void slab_connect(so2dr_ctx* ctx, const uint8_t* lower, const uint8_t* upper) {
       throw ContractError("slab_connect: blob from rank " + std::to_string(b.rank) +
                           " is not the " + (is_lower ? "lower" : "upper") + " neighbour of rank " +
                           std::to_string(sl.rank));
+    // peer access: the halo push writes the neighbour's HBM directly (NVLink
+    // / NVSwitch, or PCIe P2P). A neighbour on another GPU this process can
+    // see but not reach peer-to-peer is refused with a clear error instead of
+    // a slow or failing IPC mapping.
+    int peer_dev = -1;
+    if (cudaDeviceGetByPCIBusId(&peer_dev, b.pci) != cudaSuccess) {
+      cudaGetLastError();  // not visible here (CUDA_VISIBLE_DEVICES): IPC decides
+      peer_dev = -1;
+    }
+    e.same_device = peer_dev == ctx->device;
+    if (peer_dev >= 0 && peer_dev != ctx->device) {
+      int can = 0;
+      SO2DR_CK(cudaDeviceCanAccessPeer(&can, ctx->device, peer_dev));
+      if (!can)
+        throw ContractError("slab_connect: no peer access from GPU " + std::to_string(ctx->device) + " to GPU " +
+                            std::to_string(peer_dev) + " (" + b.pci +
+                            "): inter-slab halos need NVLink/NVSwitch or PCIe P2P");
+      e.p2p_checked = true;
+    }
     char* base = nullptr;
     if (b.pid == static_cast<uint32_t>(getpid())) {
       base = reinterpret_cast<char*>(b.raw);

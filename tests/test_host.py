@@ -282,3 +282,17 @@ def test_no_kernel_uses_local_memory():
     allowed = {"_ZN9so2dr_dev12k1_stencil3dIdLi2ELi1ELi0ELi2ELi2ELi256EEEvNS_8K1Args3DIT_EE": 128}
     bad = [(f, s) for f, _, s in funcs if int(s) > allowed.get(f, 0)]
     assert not bad, bad[:5]
+
+
+def test_pci_numa_node_sysfs_lookup(tmp_path):
+    """so2dr_device_numa_node's host logic: the GPU's PCI function's numa_node
+    file under sysfs (lower-case bus id), -1 when absent (single-node hosts
+    report -1 or 0; host_alloc then keeps cudaHostAlloc)."""
+    d = tmp_path / "bus" / "pci" / "devices" / "0000:40:00.0"
+    d.mkdir(parents=True)
+    (d / "numa_node").write_text("1\n")
+    assert so2dr.pci_numa_node("0000:40:00.0", str(tmp_path)) == 1
+    assert so2dr.pci_numa_node("0000:40:00.0".upper(), str(tmp_path)) == 1  # cudaDeviceGetPCIBusId case
+    assert so2dr.pci_numa_node("0000:41:00.0", str(tmp_path)) == -1
+    (d / "numa_node").write_text("-1\n")
+    assert so2dr.pci_numa_node("0000:40:00.0", str(tmp_path)) == -1
