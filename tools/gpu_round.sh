@@ -23,12 +23,6 @@ for s in $steps; do
     pipe)
       DS=${DS:-16,32,64} NS=${NS:-3} KS=${KS:-4,8} timeout 1200 python tools/pipe_sweep.py > $OUT/pipe_sweep.log 2>&1
       echo "pipe rc=$?" >> $OUT/summary.txt; cat $OUT/pipe_sweep.log >> $OUT/summary.txt ;;
-    ncuk1)
-      for impl in ${IMPLS:-pk p2}; do for k in ${NCU_KS:-4 8}; do
-        SO2DR_K1_IMPL=$impl timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_stencil2d -s 1 -c 1 \
-          -o $OUT/k1_${impl}_k$k -f python tools/k1_one.py $k 32768 box > $OUT/k1_${impl}_k$k.log 2>&1
-        echo "ncuk1 $impl k=$k rc=$?" >> $OUT/summary.txt
-      done; done ;;
     full)
       timeout 1500 python -m pytest tests/test_gpu_fullsize.py -x -q -m gpu --durations=0 > $OUT/pytest_fullsize.log 2>&1
       echo "fullsize rc=$?" >> $OUT/summary.txt; tail -12 $OUT/pytest_fullsize.log >> $OUT/summary.txt ;;
@@ -41,11 +35,6 @@ for s in $steps; do
     pcie)
       timeout 300 python tools/pcie_probe.py > $OUT/pcie_probe.log 2>&1; echo "pcie rc=$?" >> $OUT/summary.txt
       cat $OUT/pcie_probe.log >> $OUT/summary.txt ;;
-    p2)
-      SO2DR_K1_IMPL=p2 timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py -x -q > $OUT/pytest_p2.log 2>&1
-      echo "pytest p2 rc=$?" >> $OUT/summary.txt; tail -2 $OUT/pytest_p2.log >> $OUT/summary.txt
-      SO2DR_K1_IMPL=p2 SZ=32768 STENCILS=box2d1r,star2d1r KS=1,2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_bench_p2.log 2>&1
-      echo "k1 p2 rc=$?" >> $OUT/summary.txt; cat $OUT/k1_bench_p2.log >> $OUT/summary.txt ;;
     pcpipe)
       timeout 600 python tools/pcie_pipe.py -v > $OUT/pcie_pipe.log 2>&1; echo "pcpipe rc=$?" >> $OUT/summary.txt
       grep pattern $OUT/pcie_pipe.log >> $OUT/summary.txt ;;
@@ -77,11 +66,6 @@ for s in $steps; do
     pcpipe3)
       timeout 900 python tools/pcie_pipe3.py > $OUT/pcie_pipe3.log 2>&1; echo "pcpipe3 rc=$?" >> $OUT/summary.txt
       cat $OUT/pcie_pipe3.log >> $OUT/summary.txt ;;
-    ipw)
-      for ipw in ${IPWS:-4 8 16 32}; do for impl in ${IMPLS:-pk p2}; do
-        SO2DR_K1_IPW=$ipw SO2DR_K1_IMPL=$impl SZ=32768 STENCILS=box2d1r KS=2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_ipw${ipw}_${impl}.log 2>&1
-        echo "ipw=$ipw impl=$impl" >> $OUT/summary.txt; cat $OUT/k1_ipw${ipw}_${impl}.log >> $OUT/summary.txt
-      done; done ;;
     allocvar)
       timeout 1200 python tools/alloc_var.py > $OUT/alloc_var.log 2>&1; echo "allocvar rc=$?" >> $OUT/summary.txt
       cat $OUT/alloc_var.log >> $OUT/summary.txt ;;
@@ -105,12 +89,6 @@ for s in $steps; do
         echo "ipw=$ipw" >> $OUT/summary.txt
         tail -1 $OUT/bench_ipw$ipw.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), 'K1 ms', round(d['roofline']['avg_launch_ms'],4), 'frac', round(d['roofline']['frac'],3))" >> $OUT/summary.txt
       done ;;
-    scalar)
-      for impl in pk scalar; do
-        SO2DR_K1_IMPL=$impl SZ=32768 STENCILS=box2d1r,star2d1r KS=2,4,8 timeout 600 python tools/k1_bench.py > $OUT/k1_$impl.log 2>&1
-        echo "impl=$impl" >> $OUT/summary.txt; cat $OUT/k1_$impl.log >> $OUT/summary.txt
-      done
-      SO2DR_K1_IMPL=scalar timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q > $OUT/pytest_scalar.log 2>&1; echo "pytest scalar rc=$?" >> $OUT/summary.txt ;;
     robust)
       DS=32,64,128 NS=3,4,6 KS=4 timeout 1500 python tools/pipe_sweep.py > $OUT/pipe_sweep_robust.log 2>&1
       echo "robust rc=$?" >> $OUT/summary.txt; cat $OUT/pipe_sweep_robust.log >> $OUT/summary.txt
@@ -121,11 +99,11 @@ for s in $steps; do
       echo "robust2 rc=$?" >> $OUT/summary.txt; cat $OUT/pipe_sweep_robust2.log >> $OUT/summary.txt
       timeout 300 python tools/pipe_profile.py 92160 64 4 3 > $OUT/pp_d64.log 2>&1
       head -1 $OUT/pp_d64.log >> $OUT/summary.txt; grep -E "c(20|21|22) (htod|dtoh)" $OUT/pp_d64.log >> $OUT/summary.txt ;;
+    ncuk1)  # one in-core K1 launch per k_on: NCU_KS="1 4 8"
+      bash tools/gpu_ncuk1.sh "${NCU_KS:-4}" incore ;;
     k3d)
-      for sh in ${SHAPES:-22 42 44}; do
-        SO2DR_K1_3D=$sh SZ3=768 STENCILS=star3d1r,box3d1r KS=1,2,4 timeout 900 python tools/k1_bench.py > $OUT/k3d_$sh.log 2>&1
-        echo "shape=$sh" >> $OUT/summary.txt; cat $OUT/k3d_$sh.log >> $OUT/summary.txt
-      done
+      SZ3=768 STENCILS=star3d1r,box3d1r KS=1,2,4 timeout 900 python tools/k1_bench.py > $OUT/k3d.log 2>&1
+      echo "k3d rc=$?" >> $OUT/summary.txt; cat $OUT/k3d.log >> $OUT/summary.txt
       timeout 900 python -m pytest tests/test_gpu_3d_f64.py tests/test_gpu_fullsize.py -x -q > $OUT/pytest_3d.log 2>&1; echo "pytest 3d rc=$?" >> $OUT/summary.txt ;;
     ncu3d)
       timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_stencil3d -s 1 -c 1 -o $OUT/k1_3d_star_k4 -f \
@@ -137,22 +115,6 @@ for s in $steps; do
       timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 \
         bench.py --impl reference --gpus 2 --steps 1 --warmup 0 > $OUT/bench_ref_n2.log 2>&1
       echo "ref n2 rc=$?" >> $OUT/summary.txt; tail -1 $OUT/bench_ref_n2.log | cut -c1-300 >> $OUT/summary.txt ;;
-    v8)
-      for v in 4 8; do
-        SO2DR_K1_V=$v SZ=32768 STENCILS=box2d1r,star2d1r KS=2,4 timeout 600 python tools/k1_bench.py > $OUT/k1_v$v.log 2>&1
-        echo "V=$v" >> $OUT/summary.txt; cat $OUT/k1_v$v.log >> $OUT/summary.txt
-        SO2DR_K1_V=$v timeout 900 python bench.py --steps 3 --warmup 2 --no-cpu-baseline > $OUT/bench_v$v.log 2>&1
-        tail -1 $OUT/bench_v$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench V', $v, 'value', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), 'K1 ms', round(d['roofline']['avg_launch_ms'],4), 'frac', round(d['roofline']['frac'],3))" >> $OUT/summary.txt
-      done
-      SO2DR_K1_V=8 timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py -x -q > $OUT/pytest_v8.log 2>&1; echo "pytest v8 rc=$?" >> $OUT/summary.txt ;;
-    hyb)
-      for impl in default hyb; do
-        SO2DR_K1_IMPL=$impl SZ=32768 STENCILS=box2d1r,star2d1r,box2d2r KS=2,4,8 timeout 900 python tools/k1_bench.py > $OUT/k1_$impl.log 2>&1
-        echo "impl=$impl" >> $OUT/summary.txt; cat $OUT/k1_$impl.log >> $OUT/summary.txt
-        SO2DR_K1_IMPL=$impl timeout 900 python bench.py --steps 3 --warmup 2 --no-cpu-baseline > $OUT/bench_$impl.log 2>&1
-        tail -1 $OUT/bench_$impl.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', '$impl', 'value', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), 'K1 ms', round(d['roofline']['avg_launch_ms'],4), 'frac', round(d['roofline']['frac'],3))" >> $OUT/summary.txt
-      done
-      SO2DR_K1_IMPL=hyb timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py -x -q > $OUT/pytest_hyb.log 2>&1; echo "pytest hyb rc=$?" >> $OUT/summary.txt ;;
     ncu)
       # launch list of one bench step (e2e leg): every launch with its device time
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
