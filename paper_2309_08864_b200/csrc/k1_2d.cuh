@@ -62,11 +62,17 @@ struct K1Args2D {
   int cols;         // padded width
   int y0, y1, x0, x1;
   int iy0, iy1, ix0, ix1;
-  int seg;          // output rows per warp (y segment)
+  // Row segments (work items = unit x segment, DESIGN.md 4 "guided items"):
+  // units that own ring columns take uniform segments of seg_e rows; inner
+  // units take nseg_b big segments of seg_b rows from y0, then the rest of
+  // the rows in small segments of seg_s (handed out last: they fill the
+  // launch tail)
+  int seg_e, nseg_e;
+  int seg_b, nseg_b;
+  int seg_s, nseg_s;
   int strip;        // output columns per warp
   int xorg;         // column of lane 0 cell 0 of warp 0 (aligned to VEC)
   int warps_x;      // strips along x
-  int nseg;         // row segments; work items = warps_x * nseg
   int nl, nr;       // leading / trailing strips that own ring columns (slow path)
   int gnl, gnr;     // the same in strip groups (CTA items of the streaming path)
   int cpb;          // cp.async piece bytes (16/8/4): largest dividing the pitch
@@ -259,7 +265,7 @@ struct K1Plan2D {
 // One work item = (strip wx, row segment sg) processed by one warp; `wring`
 // is the warp's shared ring (each lane uses its own slots only).
 template <typename T, int R, int S, int KIND, int V, int NT, bool SCALAR = false>
-__device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg, T* wring) {
+__device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int OY0, int OY1, T* wring) {
   using P = K1Plan2D<T, R, S, KIND, V, NT>;
   constexpr int E = P::E, H = P::H, VEC = P::VEC;
   constexpr int kRing = P::RING;
@@ -270,8 +276,6 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg, T*
   const int wc0 = a.xorg + wx * a.strip;  // column of lane 0 cell 0
   const int OX0 = max(wc0 + P::HS, a.x0);
   const int OX1 = min(wc0 + P::HS + a.strip, a.x1);
-  const int OY0 = a.y0 + sg * a.seg;
-  const int OY1 = min(OY0 + a.seg, a.y1);
   const int sy0 = a.base, sy1 = a.base + a.rows;
   const int lo0 = max(OY0 - H, sy0), hi0 = min(OY1 + H, sy1);
   const int n_iter = OY1 - lo0 + S * (R + 1);
@@ -530,27 +534,49 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int sg, T*
 }
 
 
-// Work item -> (strip, segment). The strips that own ring columns run the
-// general (range-checked) path for their whole height and cost several times
-// a steady-state item, so they are handed out FIRST (longest items first):
+// Work item -> (strip, output rows [oy0, oy1)). The strips that own ring
+// columns run the range-checked edge pipeline and cost several times a
+// steady-state item, so they are handed out FIRST (longest items first):
 // fetched last they left one SM running alone for ~25% of the launch
-// (profiles/r01_baseline/k1_full.json: SM active avg 73.5% of elapsed).
+// (profiles/r01_baseline/k1_full.json: SM active avg 73.5% of elapsed). The
+// inner units' big segments come next and their small segments last, so the
+// launch ends on short items (k1_plan_segments).
 template <typename T>
-__device__ __forceinline__ void k1_item_coords(const K1Args2D<T>& a, int item, int& wx, int& sg, int units) {
+__device__ __forceinline__ int k1_items_total(const K1Args2D<T>& a, int units) {
+  const int nl = units == a.warps_x ? a.nl : a.gnl, nr = units == a.warps_x ? a.nr : a.gnr;
+  const int ne = nl + nr;
+  return ne * a.nseg_e + (units - ne) * (a.nseg_b + a.nseg_s);
+}
+
+template <typename T>
+__device__ __forceinline__ void k1_item_coords(const K1Args2D<T>& a, int item, int& wx, int& oy0, int& oy1,
+                                               int units) {
   // units: strips (per-warp items) or strip groups (CTA items); the leading /
   // trailing units that own ring columns come first
   const int nl = units == a.warps_x ? a.nl : a.gnl, nr = units == a.warps_x ? a.nr : a.gnr;
   const int ne = nl + nr;
-  if (item < ne * a.nseg) {
-    sg = item / ne;
+  if (item < ne * a.nseg_e) {
+    const int sg = item / ne;
     const int j = item - sg * ne;
     wx = j < nl ? j : units - ne + j;
-  } else {
-    const int inner = units - ne;
-    const int i = item - ne * a.nseg;
-    sg = i / inner;
-    wx = nl + (i - sg * inner);
+    oy0 = a.y0 + sg * a.seg_e;
+    oy1 = min(oy0 + a.seg_e, a.y1);
+    return;
   }
+  const int inner = units - ne;
+  int i = item - ne * a.nseg_e;
+  if (i < inner * a.nseg_b) {
+    const int sg = i / inner;
+    wx = nl + (i - sg * inner);
+    oy0 = a.y0 + sg * a.seg_b;
+    oy1 = min(oy0 + a.seg_b, a.y1);
+    return;
+  }
+  i -= inner * a.nseg_b;
+  const int sg = i / inner;
+  wx = nl + (i - sg * inner);
+  oy0 = a.y0 + a.nseg_b * a.seg_b + sg * a.seg_s;
+  oy1 = min(oy0 + a.seg_s, a.y1);
 }
 
 }  // namespace so2dr_dev
@@ -597,19 +623,17 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
     gr.rowb = P::CTA_ROWB;
     unsigned g_it = 0;  // CTA-ring slots consumed (identical in every warp)
     const int groups = (a.warps_x + NW - 1) / NW;
-    const int total = groups * a.nseg;
+    const int total = k1_items_total(a, groups);
     for (;;) {
       __syncthreads();  // every warp done with the previous item (and s_item)
       if (threadIdx.x == 0) s_item = static_cast<int>(atomicAdd(a.counter, 1u));
       __syncthreads();
       const int item = s_item;
       if (item >= total) break;
-      int gx, sg;
-      k1_item_coords(a, item, gx, sg, groups);
+      int gx, OY0, OY1;
+      k1_item_coords(a, item, gx, OY0, OY1, groups);
       const int wx0 = gx * NW;
       const int wc0 = a.xorg + wx0 * a.strip;
-      const int OY0 = a.y0 + sg * a.seg;
-      const int OY1 = min(OY0 + a.seg, a.y1);
       // inner group: NW whole strips, no pass-through cell, rows stage 1 emits
       // (the widest stage range) all interior, 8-byte aligned rows, output
       // columns on lane boundaries, and the bulk copy's 16-byte slack inside
@@ -623,9 +647,9 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
                          lanes_whole;
       if (inner) {
         gr.wcg = wc0;
-        k1_item_stream<T, R, S, KIND, V, NT, kModeGroup>(a, wx0 + warp, sg, wring, gr, g_it);
+        k1_item_stream<T, R, S, KIND, V, NT, kModeGroup>(a, wx0 + warp, OY0, OY1, wring, gr, g_it);
       } else if (wx0 + warp < a.warps_x) {
-        k1_item_stream<T, R, S, KIND, V, NT, kModeEdge>(a, wx0 + warp, sg, wring, gr, g_it);
+        k1_item_stream<T, R, S, KIND, V, NT, kModeEdge>(a, wx0 + warp, OY0, OY1, wring, gr, g_it);
       }
     }
     if (threadIdx.x == 0) {
@@ -640,26 +664,24 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
     // per-warp work items = (strip, row segment) on the streaming path
     GroupRing gr{};
     unsigned g_it = 0;
-    const int total = a.warps_x * a.nseg;
+    const int total = k1_items_total(a, a.warps_x);
     for (;;) {
       int item = 0;
       if (lane == 0) item = static_cast<int>(atomicAdd(a.counter, 1u));
       item = __shfl_sync(0xffffffffu, item, 0);
       if (item >= total) break;
-      int wx, sg;
-      k1_item_coords(a, item, wx, sg, a.warps_x);
+      int wx, OY0, OY1;
+      k1_item_coords(a, item, wx, OY0, OY1, a.warps_x);
       const int wc0 = a.xorg + wx * a.strip;
-      const int OY0 = a.y0 + sg * a.seg;
-      const int OY1 = min(OY0 + a.seg, a.y1);
       const int lo1 = max(OY0 - (H - R), a.base), hi1 = min(OY1 + (H - R), a.base + a.rows);
       const int OX0 = max(wc0 + P::HS, a.x0), OX1 = min(wc0 + P::HS + a.strip, a.x1);
       const bool lanes_whole = OX0 >= OX1 || ((OX0 - wc0) % V == 0 && (OX1 - wc0) % V == 0);
       const bool inner = wc0 >= a.ix0 && wc0 + 32 * V <= a.ix1 && lo1 >= a.iy0 && hi1 <= a.iy1 && a.aligned8 &&
                          lanes_whole;
       if (inner)
-        k1_item_stream<T, R, S, KIND, V, NT, kModeLane>(a, wx, sg, wring, gr, g_it);
+        k1_item_stream<T, R, S, KIND, V, NT, kModeLane>(a, wx, OY0, OY1, wring, gr, g_it);
       else
-        k1_item_stream<T, R, S, KIND, V, NT, kModeEdge>(a, wx, sg, wring, gr, g_it);
+        k1_item_stream<T, R, S, KIND, V, NT, kModeEdge>(a, wx, OY0, OY1, wring, gr, g_it);
     }
     if (lane == 0) {
       __threadfence();
@@ -672,15 +694,15 @@ __global__ void __launch_bounds__(NT, MINB) k1_stencil2d(const K1Args2D<T> a) {
     }
   } else {
     // per-warp work items = (strip, row segment): general path
-    const int total = a.warps_x * a.nseg;
+    const int total = k1_items_total(a, a.warps_x);
     for (;;) {
       int item = 0;
       if (lane == 0) item = static_cast<int>(atomicAdd(a.counter, 1u));
       item = __shfl_sync(0xffffffffu, item, 0);
       if (item >= total) break;
-      int wx, sg;
-      k1_item_coords(a, item, wx, sg, a.warps_x);
-      k1_item<T, R, S, KIND, V, NT, true>(a, wx, sg, wring);
+      int wx, OY0, OY1;
+      k1_item_coords(a, item, wx, OY0, OY1, a.warps_x);
+      k1_item<T, R, S, KIND, V, NT, true>(a, wx, OY0, OY1, wring);
     }
     // The last warp to leave re-arms the counter pair for the next launch
     // that uses it (no memset per launch).

@@ -10,6 +10,7 @@
 
 #include "k1_2d.cuh"
 #include "k1_launch.h"
+#include "k1_segplan.h"
 
 namespace so2dr_dev {
 
@@ -46,16 +47,22 @@ constexpr int minb2d(int R, int S) {
 
 inline int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
-// Work items per resident warp (row segments x strips): more items balance
-// the tail, longer segments amortise the R*S warm-up rows and the pipeline
-// fill. SO2DR_K1_IPW=n overrides (experiments).
-inline int k1_items_per_warp(int height) {
+// Work items per resident warp (row segments x strips) for the uniform
+// segmentation (SO2DR_K1_IPW=n: experiments / A-B against the guided plan).
+inline int k1_items_per_warp_override() {
   static int v = [] {
     const char* s = std::getenv("SO2DR_K1_IPW");
     return s ? std::max(1, std::atoi(s)) : 0;
   }();
-  if (v) return v;
-  return height < 4096 ? 4 : 6;
+  return v;
+}
+// SO2DR_K1_SEGS=uniform: the r02-mid uniform segmentation (A/B experiments)
+inline bool k1_uniform_segments() {
+  static bool v = [] {
+    const char* s = std::getenv("SO2DR_K1_SEGS");
+    return s && std::strcmp(s, "uniform") == 0;
+  }();
+  return v;
 }
 
 template <typename T, int R, int S, int KIND, int V>
@@ -133,20 +140,38 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   }
   const int sms = device_sm_count();
   const int resident_warps = sms * occ * NW;
-  const int min_seg = std::max(32, 4 * (2 * H + 2 * S * ((R + 1) / 2)));
-  const int max_ns = std::max(1, height / min_seg);
   // streaming shapes hand out CTA items (strip groups of NW strips), the
   // general path warp items (strips)
   constexpr bool kGroup = KIND != KGRAD && !(sizeof(T) == 8 && R >= 3) && P::GROUPED;
+  constexpr bool kStreamPath = KIND != KGRAD && !(sizeof(T) == 8 && R >= 3);
   const int units = kGroup ? (a.warps_x + NW - 1) / NW : a.warps_x;
+  const int edge_units = kGroup ? a.gnl + a.gnr : a.nl + a.nr;
   const int workers = kGroup ? sms * occ : resident_warps;
-  int ns = std::max(1, (k1_items_per_warp(height) * workers + units - 1) / units);
-  ns = std::min(ns, max_ns);
-  a.seg = (height + ns - 1) / ns;
-  a.nseg = (height + a.seg - 1) / a.seg;
+  // uniform segments: ipw items per worker, each >= 4x its warm-up
+  const int min_seg_u = std::max(32, 4 * (2 * H + 2 * S * ((R + 1) / 2)));
+  const int ipw = k1_items_per_warp_override() ? k1_items_per_warp_override() : (height < 4096 ? 4 : 6);
+  const int ns_u = std::min(std::max(1, (ipw * workers + units - 1) / units), std::max(1, height / min_seg_u));
+  const int seg_u = std::max(1, (height + ns_u - 1) / ns_u);
+  if (k1_items_per_warp_override() || k1_uniform_segments()) {
+    a.seg_e = a.seg_b = a.seg_s = seg_u;
+    a.nseg_e = a.nseg_b = (height + seg_u - 1) / seg_u;
+    a.nseg_s = 0;
+  } else {
+    // guided: the same or shorter segments, the tail cut finer. Rows an item
+    // recomputes besides its own: H warm-up rows, the pipeline fill
+    // (2*ceil(R/2) rows per stage streaming, R+1 general) and ~6 rows' worth
+    // of per-item setup latency
+    const int ov = H + (kStreamPath ? 2 * S * ((R + 1) / 2) : S * (R + 1)) + 6;
+    const K1SegPlan sp = k1_plan_segments(height, units, edge_units >= units ? units : edge_units, workers, ov,
+                                          4.5, std::max(16, 2 * ov), seg_u);
+    a.seg_e = sp.seg_e, a.nseg_e = sp.nseg_e;
+    a.seg_b = sp.seg_b, a.nseg_b = sp.nseg_b;
+    a.seg_s = sp.seg_s, a.nseg_s = sp.nseg_s;
+  }
   a.counter = k1_next_counter(stream);
   if (!a.counter) return cudaErrorUnknown;
-  const int items = units * a.nseg;
+  const int ne = edge_units >= units ? units : edge_units;
+  const int items = ne * a.nseg_e + (units - ne) * (a.nseg_b + a.nseg_s);
   const int ctas = std::max(1, std::min(sms * occ, kGroup ? items : (items + NW - 1) / NW));
   kern<<<ctas, NT, 0, stream>>>(a);
   return cudaGetLastError();

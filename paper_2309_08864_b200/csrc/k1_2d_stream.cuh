@@ -181,7 +181,7 @@ enum : int {
 };
 
 template <typename T, int R, int S, int KIND, int V, int NT, int MODE>
-__device__ __forceinline__ void k1_item_stream(const K1Args2D<T>& a, int wx, int sg, T* wring, const GroupRing& gr,
+__device__ __forceinline__ void k1_item_stream(const K1Args2D<T>& a, int wx, int OY0, int OY1, T* wring, const GroupRing& gr,
                                                unsigned& g_it) {
   using P = K1Plan2D<T, R, S, KIND, V, NT>;
   using SP = StreamPlan2D<T, R, KIND>;
@@ -201,8 +201,6 @@ __device__ __forceinline__ void k1_item_stream(const K1Args2D<T>& a, int wx, int
   const int wc0 = a.xorg + wx * a.strip;
   const int OX0 = max(wc0 + P::HS, a.x0);
   const int OX1 = min(wc0 + P::HS + a.strip, a.x1);
-  const int OY0 = a.y0 + sg * a.seg;
-  const int OY1 = min(OY0 + a.seg, a.y1);
   const int sy0 = a.base, sy1 = a.base + a.rows;
   const int lo0 = max(OY0 - H, sy0), hi0 = min(OY1 + H, sy1);
   const int n_iter = (OY1 - lo0 + 2 * C * S + 1) / 2;

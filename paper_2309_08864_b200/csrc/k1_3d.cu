@@ -30,6 +30,7 @@
 
 #include "k1_2d.cuh"  // fma_rn, cp_async helpers
 #include "k1_launch.h"
+#include "k1_segplan.h"
 
 #ifndef SO2DR_K3D_SHAPE  // fp32 radius-1 cells per thread: 22 = 2x2 on 512 threads, 24 = 2x4 on 256
 #define SO2DR_K3D_SHAPE 22
@@ -48,11 +49,12 @@ struct K1Args3D {
   int z0, z1;            // output planes
   int iz0, iz1;          // interior planes
   int i0, i1;            // in-plane interior [i0, i1) for y and x
-  int seg;               // output planes per CTA
+  int seg_b, nseg_b;     // z segments: nseg_b big ones of seg_b planes from z0,
+  int seg_s, nseg_s;     // then small ones of seg_s (handed out last: k1_plan_segments)
   int tile_x, tile_y;    // valid output cells per CTA along x / y
   int xorg, yorg;        // origin of CTA (0,0)'s thread cell (aligned)
   int cpb;               // cp.async piece bytes (largest of 16/8/4 dividing the pitch)
-  int nx, ny, nz;        // tiles along x / y, z segments (work items nx*ny*nz)
+  int nx, ny;            // tiles along x / y (work items nx*ny*(nseg_b+nseg_s))
   unsigned* counter;     // work-item counter pair (k1_next_counter)
   T w[125];              // (2R+1)^3 canonical weights
 };
@@ -65,7 +67,8 @@ struct K1Args3D {
 // read buffer's value (a CTA-uniform test per plane); tiles that hang over the
 // padded grid load with per-element range checks.
 template <typename T, int R, int S, int KIND, int V, int VY, int NT>
-__device__ __forceinline__ void k1_tile3d(const K1Args3D<T>& a, int tx, int ty, int tz, unsigned char* smem_raw) {
+__device__ __forceinline__ void k1_tile3d(const K1Args3D<T>& a, int tx, int ty, int OZ0, int OZ1,
+                                          unsigned char* smem_raw) {
   constexpr int E = 2 * R + 1, H = R * S, NW = NT / 32;
   constexpr int RING = 4;
   using Ring = T[RING][VY][NT * V];
@@ -78,8 +81,6 @@ __device__ __forceinline__ void k1_tile3d(const K1Args3D<T>& a, int tx, int ty, 
   const int cy0 = a.yorg + ty * a.tile_y;  // y of warp 0 row 0
   const int xt = cx0 + lane * V;
   const int yt = cy0 + warp * VY;
-  const int OZ0 = a.z0 + tz * a.seg;
-  const int OZ1 = min(OZ0 + a.seg, a.z1);
   const int sz0 = a.base, sz1 = a.base + a.planes;
   const int lo0 = max(OZ0 - H, sz0), hi0 = min(OZ1 + H, sz1);
   const int n_iter = OZ1 - lo0 + S * (R + 1);
@@ -295,16 +296,26 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
   // the guard warps' edge rows (above warp 0 / below the last warp) are never
   // written: zero them once (finite garbage for the tile's outer halo)
   for (int i = threadIdx.x; i < 2 * S * (NW + 2) * 2 * R * 32 * V; i += NT) (&yedge[0][0][0][0][0][0])[i] = T(0);
-  const int total = a.nx * a.ny * a.nz;
+  const int tiles = a.nx * a.ny;
+  const int total = tiles * (a.nseg_b + a.nseg_s);
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_item = static_cast<int>(atomicAdd(a.counter, 1u));
     __syncthreads();
     const int item = s_item;
     if (item >= total) break;
-    const int tz = item / (a.nx * a.ny), rem = item - tz * a.nx * a.ny;
+    int tz = item / tiles;
+    const int rem = item - tz * tiles;
     const int ty = rem / a.nx, tx = rem - ty * a.nx;
-    k1_tile3d<T, R, S, KIND, V, VY, NT>(a, tx, ty, tz, smem_raw);
+    int oz0;
+    if (tz < a.nseg_b) {
+      oz0 = a.z0 + tz * a.seg_b;
+    } else {
+      tz -= a.nseg_b;
+      oz0 = a.z0 + a.nseg_b * a.seg_b + tz * a.seg_s;
+    }
+    const int oz1 = min(oz0 + (item < tiles * a.nseg_b ? a.seg_b : a.seg_s), a.z1);
+    k1_tile3d<T, R, S, KIND, V, VY, NT>(a, tx, ty, oz0, oz1, smem_raw);
   }
   if (threadIdx.x == 0) {
     __threadfence();
@@ -371,16 +382,8 @@ cudaError_t launch3(const K1Launch& L, cudaStream_t stream) {
   const int ny = (a.p - (a.yorg + H) + a.tile_y - 1) / a.tile_y;
   const int depth = L.y1 - L.y0;
   const int sms = device_sm_count();
-  const int min_seg = std::max(16, 4 * (H + S * (R + 1)));
-  int nz = std::max(1, (8 * sms + nx * ny - 1) / (nx * ny));
-  nz = std::min(nz, std::max(1, depth / min_seg));
-  a.seg = (depth + nz - 1) / nz;
-  nz = (depth + a.seg - 1) / a.seg;
   a.nx = nx;
   a.ny = ny;
-  a.nz = nz;
-  a.counter = k1_next_counter(stream);
-  if (!a.counter) return cudaErrorUnknown;
   static int occ_by_dev[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
@@ -389,7 +392,21 @@ cudaError_t launch3(const K1Launch& L, cudaStream_t stream) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem) != cudaSuccess || occ < 1) occ = 1;
     occ_by_dev[dev] = occ;
   }
-  const int ctas = std::max(1, std::min(sms * occ, nx * ny * nz));
+  // z segmentation: guided plan over the persistent CTAs (big segments, then
+  // small ones that even out the finish times); an item recomputes its H
+  // warm-up planes and the S(R+1)-plane pipeline fill
+  const int ov = H + S * (R + 1) + 4;
+  const int min_seg_u = std::max(16, 4 * (H + S * (R + 1)));  // r02-mid: ~8 items per SM
+  int nz_u = std::max(1, (8 * sms + nx * ny - 1) / (nx * ny));
+  nz_u = std::min(nz_u, std::max(1, depth / min_seg_u));
+  const int seg_u = std::max(1, (depth + nz_u - 1) / nz_u);
+  const K1SegPlan sp = k1_plan_segments(depth, nx * ny, 0, (int64_t)sms * occ, ov, 1.0, std::max(8, 2 * ov), seg_u);
+  a.seg_b = sp.seg_b, a.nseg_b = sp.nseg_b;
+  a.seg_s = sp.seg_s, a.nseg_s = sp.nseg_s;
+  const int64_t items = (int64_t)nx * ny * (a.nseg_b + a.nseg_s);
+  a.counter = k1_next_counter(stream);
+  if (!a.counter) return cudaErrorUnknown;
+  const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, items));
   kern<<<ctas, NT, smem, stream>>>(a);
   return cudaGetLastError();
 }
