@@ -145,33 +145,51 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def pcie_probe(torch, dev):
+def pcie_probe(torch, dev, eng=None):
     """Pinned-host PCIe GB/s on this box, timed with CUDA events on the copy
-    streams: H2D alone, D2H alone, and both at once (2 GiB each way). In duplex
-    the host side caps the COMBINED rate (~94 GB/s here, tools/pcie_probe.py),
-    so duplex_GBps_per_dir = combined / 2 is what a balanced pipeline can use."""
+    streams: H2D alone, D2H alone, and both at once (2 GiB each way, as 8 copies
+    of 256 MiB per direction, best of 3). In duplex the host side caps the
+    COMBINED rate (~94 GB/s here, tools/pcie_probe.py), so duplex_GBps_per_dir =
+    combined / 2 is what a balanced pipeline can use. The host buffers come from
+    the engine's own allocator (so2dr_host_alloc, as the bench grid) when torch
+    sees them as pinned, else from torch's pinned allocator (the line says which)."""
     n = 2 << 30
-    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    pieces = 8
+    src = "torch pin_memory"
+    h = h2 = None
+    if eng is not None:
+        try:
+            ha = torch.from_numpy(eng.host_array((n,), np.uint8))
+            hb = torch.from_numpy(eng.host_array((n,), np.uint8))
+            if ha.is_pinned() and hb.is_pinned():
+                h, h2, src = ha, hb, "so2dr_host_alloc"
+        except Exception:  # noqa: BLE001 - fall back to torch's pinned memory
+            h = h2 = None
+    if h is None:
+        h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(n, dtype=torch.uint8, device=dev)
     d2 = torch.empty(n, dtype=torch.uint8, device=dev)
     s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     out = {}
+    step = n // pieces
     for name in ("h2d", "d2h", "duplex"):
         best = 0.0
-        for _ in range(2):
+        for _ in range(3):
             torch.cuda.synchronize(dev)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
             s1.wait_event(e0)
             s2.wait_event(e0)
-            if name in ("h2d", "duplex"):
-                with torch.cuda.stream(s1):
-                    d.copy_(h, non_blocking=True)
-            if name in ("d2h", "duplex"):
-                with torch.cuda.stream(s2):
-                    h2.copy_(d2, non_blocking=True)
+            for i in range(pieces):
+                sl = slice(i * step, (i + 1) * step)
+                if name in ("h2d", "duplex"):
+                    with torch.cuda.stream(s1):
+                        d[sl].copy_(h[sl], non_blocking=True)
+                if name in ("d2h", "duplex"):
+                    with torch.cuda.stream(s2):
+                        h2[sl].copy_(d2[sl], non_blocking=True)
             torch.cuda.current_stream().wait_stream(s1)
             torch.cuda.current_stream().wait_stream(s2)
             e1.record()
@@ -180,6 +198,7 @@ def pcie_probe(torch, dev):
             best = max(best, moved / e0.elapsed_time(e1) / 1e6)
         out[name + ("_combined_GBps" if name == "duplex" else "_GBps")] = round(best, 2)
     out["duplex_GBps_per_dir"] = round(out["duplex_combined_GBps"] / 2, 2)
+    out["host_buffers"] = src
     del h, h2, d, d2
     return out
 
@@ -457,12 +476,12 @@ def main():
     t_reg = time.perf_counter() - t0
     eng.init_rows(sz, R, 42, lo, hi, host)
     connect()
-    pc = pcie_probe(torch, dev) if rank == 0 and args.pcie_probe_before else {}
+    pc = pcie_probe(torch, dev, eng) if rank == 0 and args.pcie_probe_before else {}
     with ClockSampler(dev_index, args.clock_ms) as clk:
         e2e_res = leg(host, args.steps, args.warmup)
     clocks = clk.summary()
     if rank == 0 and not args.pcie_probe_before:
-        pc = pcie_probe(torch, dev)
+        pc = pcie_probe(torch, dev, eng)
     # multi-GPU evidence: every rank's own e2e time, its GPU's NUMA node and the
     # halo transport of its slab edges (all ranks take part in the gather)
     mine = {"rank": rank, "device_ms": e2e_res["rank_ms"], "numa_node": so2dr.device_numa_node(dev_index),

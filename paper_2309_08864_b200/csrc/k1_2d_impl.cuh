@@ -47,8 +47,9 @@ constexpr int minb2d(int R, int S) {
 
 inline int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
-// Work items per resident warp (row segments x strips) for the uniform
-// segmentation (SO2DR_K1_IPW=n: experiments / A-B against the guided plan).
+// Work items per resident warp (row segments x strips) of the uniform
+// segmentation, which also caps the guided plan's segment length
+// (SO2DR_K1_IPW=n: experiments).
 inline int k1_items_per_warp_override() {
   static int v = [] {
     const char* s = std::getenv("SO2DR_K1_IPW");
@@ -149,10 +150,10 @@ cudaError_t launch_2d_fixed(const K1Launch& L, cudaStream_t stream) {
   const int workers = kGroup ? sms * occ : resident_warps;
   // uniform segments: ipw items per worker, each >= 4x its warm-up
   const int min_seg_u = std::max(32, 4 * (2 * H + 2 * S * ((R + 1) / 2)));
-  const int ipw = k1_items_per_warp_override() ? k1_items_per_warp_override() : (height < 4096 ? 4 : 6);
+  const int ipw = k1_items_per_warp_override() ? k1_items_per_warp_override() : 8;  // profiles/r02_guided/ipw_ab.txt
   const int ns_u = std::min(std::max(1, (ipw * workers + units - 1) / units), std::max(1, height / min_seg_u));
   const int seg_u = std::max(1, (height + ns_u - 1) / ns_u);
-  if (k1_items_per_warp_override() || k1_uniform_segments()) {
+  if (k1_uniform_segments()) {
     a.seg_e = a.seg_b = a.seg_s = seg_u;
     a.nseg_e = a.nseg_b = (height + seg_u - 1) / seg_u;
     a.nseg_s = 0;

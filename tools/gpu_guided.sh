@@ -1,5 +1,5 @@
 # A/B of the K1 row segmentation: guided plan (default) vs the r02-mid uniform
-# segments (SO2DR_K1_SEGS=uniform: 4 items per warp below 4096 rows, 6 above).
+# segments (SO2DR_K1_SEGS=uniform: SO2DR_K1_IPW items per warp, r02-mid: 4 below 4096 rows, 6 above).
 #   gpurun -- 'bash tools/gpu_guided.sh [tests]'
 OUT=gpurun_out; mkdir -p $OUT; rm -f $OUT/summary.txt
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $OUT/smi.txt 2>&1
