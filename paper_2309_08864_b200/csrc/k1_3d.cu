@@ -66,7 +66,7 @@ struct K1Args3D {
 // columns): after every stage the emitted plane's ring cells are reset to the
 // read buffer's value (a CTA-uniform test per plane); tiles that hang over the
 // padded grid load with per-element range checks.
-template <typename T, int R, int S, int KIND, int V, int VY, int NT>
+template <typename T, int R, int S, int KIND, int V, int VY, int NT, bool EDGE>
 __device__ __forceinline__ void k1_tile3d(const K1Args3D<T>& a, int tx, int ty, int OZ0, int OZ1,
                                           unsigned char* smem_raw) {
   constexpr int E = 2 * R + 1, H = R * S, NW = NT / 32;
@@ -104,7 +104,8 @@ __device__ __forceinline__ void k1_tile3d(const K1Args3D<T>& a, int tx, int ty, 
     }
   // every cell of the tile inside the padded grid: loads need no per-element
   // range checks (CTA-uniform)
-  const bool xy_inside = cx0 >= 0 && cx0 + 32 * V <= a.p && cy0 >= 0 && cy0 + NW * VY <= a.p;
+  // (EDGE = false: the caller checked that the whole tile is interior in x-y)
+  const bool xy_inside = !EDGE || (cx0 >= 0 && cx0 + 32 * V <= a.p && cy0 >= 0 && cy0 + NW * VY <= a.p);
 
   T cur[S][VY][V];
   T acc[S][E][VY][V];
@@ -126,7 +127,7 @@ __device__ __forceinline__ void k1_tile3d(const K1Args3D<T>& a, int tx, int ty, 
     if (plane < hi0) {
 #pragma unroll
       for (int j = 0; j < VY; ++j) {
-        if (!xy_inside) {
+        if (EDGE && !xy_inside) {
           const int y = yt + j;
           if (y >= 0 && y < a.p) {
             const T* src = a.in + (int64_t)(plane - sz0) * a.plane_stride + (int64_t)y * a.pitch;
@@ -148,10 +149,21 @@ __device__ __forceinline__ void k1_tile3d(const K1Args3D<T>& a, int tx, int ty, 
 
   // CTA-uniform: does this item own any pass-through cell (ring column/row of
   // the tile, or a ring plane in the z range its stages emit)?
-  const bool tile_edge = __syncthreads_or(ringmask != 0) || lo0 - H < a.iz0 || OZ1 + H > a.iz1;
+  // Interior tiles (EDGE = false) own no ring column / row: only the ring
+  // planes pass through, and every cell of the tile is inside the grid.
+  const bool tile_edge = (EDGE && __syncthreads_or(ringmask != 0)) || lo0 - H < a.iz0 || OZ1 + H > a.iz1;
   auto passthru = [&](int plane, T (&v)[VY][V]) SO2DR_INLINE {
     if (plane < sz0 || plane >= sz1) return;
     const bool ring_plane = plane < a.iz0 || plane >= a.iz1;
+    if constexpr (!EDGE) {
+      if (!ring_plane) return;
+      const T* g = a.in + (int64_t)(plane - sz0) * a.plane_stride + yx;
+#pragma unroll
+      for (int j = 0; j < VY; ++j)
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[j][k] = __ldg(g + (int64_t)j * a.pitch + k);
+      return;
+    }
     const unsigned m = ring_plane ? inmask : ringmask;
     if (!m) return;
     const T* g = a.in + (int64_t)(plane - sz0) * a.plane_stride + yx;
@@ -315,7 +327,18 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
       oz0 = a.z0 + a.nseg_b * a.seg_b + tz * a.seg_s;
     }
     const int oz1 = min(oz0 + (item < tiles * a.nseg_b ? a.seg_b : a.seg_s), a.z1);
-    k1_tile3d<T, R, S, KIND, V, VY, NT>(a, tx, ty, oz0, oz1, smem_raw);
+    // x-y interior tile: no ring cell, no cell off the grid (CTA-uniform)
+    const int cx0 = a.xorg + tx * a.tile_x, cy0 = a.yorg + ty * a.tile_y;
+    // One variant only where two inlined pipelines do not fit: fp64 radius 2
+    // (the state spills) and the long box bodies (> 64 fmas per cell and
+    // iteration: the doubled loop code misses the instruction cache -- box3d1r
+    // k=4 measured -11% with both, k=2 +9%)
+    constexpr int kTaps = KIND == KBOX ? (2 * R + 1) * (2 * R + 1) * (2 * R + 1) : 6 * R + 1;
+    constexpr bool kInnerVariant = !(sizeof(T) == 8 && R == 2) && S * kTaps <= 64;
+    if (kInnerVariant && cx0 >= a.i0 && cx0 + 32 * V <= a.i1 && cy0 >= a.i0 && cy0 + NW * VY <= a.i1)
+      k1_tile3d<T, R, S, KIND, V, VY, NT, false>(a, tx, ty, oz0, oz1, smem_raw);
+    else
+      k1_tile3d<T, R, S, KIND, V, VY, NT, true>(a, tx, ty, oz0, oz1, smem_raw);
   }
   if (threadIdx.x == 0) {
     __threadfence();
