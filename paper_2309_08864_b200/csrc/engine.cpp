@@ -17,16 +17,34 @@
 // D2H of different chunks overlap on the two copy engines and the SMs.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
 
 #include "engine.h"
+
+
+// NVTX ranges over the host-side enqueue of a run / round / chunk (SURVEY 5:
+// tracing). Header-only NVTX v3: a few ns per range unless a tool (nsys,
+// ncu --nvtx) injects itself.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* fmt, int a, int b) {
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), fmt, a, b);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace so2dr {
 std::string next_share_buffer_id();  // host_model.cpp
@@ -698,6 +716,7 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
               ev_hi_used = nullptr;
 
   for (int t = 0; t < rp.rounds; ++t) {
+    NvtxRange nv_round("so2dr round %d (%d steps)", t, rp.steps_in_round(t));
     const int k_eff = rp.steps_in_round(t);
     const int calls = rp.calls_in_round(t);
     const uint32_t epoch = static_cast<uint32_t>(sl.epoch);
@@ -731,6 +750,7 @@ void run_so2dr(RunCtx& rc, const RunRequest& q, const so2dr::RunConfig& cfg, Acc
     }
 
     for (int i = cb; i < ce; ++i) {
+      NvtxRange nv_chunk("so2dr chunk %d round %d", i, t);
       const so2dr::ChunkIntervals& ci = lay.chunks[i];
       const int pk = (i - cb) % ns;
       Field& f = F[pk];
@@ -1108,6 +1128,8 @@ void run(so2dr_ctx* ctx, RunRequest& q, RunResponse& out) {
   for (int k = 1; k < nstreams; ++k) wait(ctx->stream(k), ev_start);
 
   try {
+    NvtxRange nv_run(q.mode == SO2DR_MODE_SO2DR ? "so2dr_run so2dr" : q.mode == SO2DR_MODE_INCORE ? "so2dr_run incore"
+                                                                                               : "so2dr_run resreu");
     switch (q.mode) {
       case SO2DR_MODE_SO2DR: run_so2dr(rc, q, cfg, acc, rec); break;
       case SO2DR_MODE_INCORE: run_incore(rc, q, cfg, acc, rec); break;

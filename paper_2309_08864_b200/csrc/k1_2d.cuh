@@ -50,6 +50,7 @@
 #include <utility>
 
 #include "k1_launch.h"
+#include "k1_segplan.h"
 
 namespace so2dr_dev {
 
@@ -544,8 +545,7 @@ __device__ __forceinline__ void k1_item(const K1Args2D<T>& a, int wx, int OY0, i
 template <typename T>
 __device__ __forceinline__ int k1_items_total(const K1Args2D<T>& a, int units) {
   const int nl = units == a.warps_x ? a.nl : a.gnl, nr = units == a.warps_x ? a.nr : a.gnr;
-  const int ne = nl + nr;
-  return ne * a.nseg_e + (units - ne) * (a.nseg_b + a.nseg_s);
+  return k1_seg_items(K1SegPlan{a.seg_e, a.nseg_e, a.seg_b, a.nseg_b, a.seg_s, a.nseg_s}, units, nl + nr);
 }
 
 template <typename T>
@@ -554,29 +554,8 @@ __device__ __forceinline__ void k1_item_coords(const K1Args2D<T>& a, int item, i
   // units: strips (per-warp items) or strip groups (CTA items); the leading /
   // trailing units that own ring columns come first
   const int nl = units == a.warps_x ? a.nl : a.gnl, nr = units == a.warps_x ? a.nr : a.gnr;
-  const int ne = nl + nr;
-  if (item < ne * a.nseg_e) {
-    const int sg = item / ne;
-    const int j = item - sg * ne;
-    wx = j < nl ? j : units - ne + j;
-    oy0 = a.y0 + sg * a.seg_e;
-    oy1 = min(oy0 + a.seg_e, a.y1);
-    return;
-  }
-  const int inner = units - ne;
-  int i = item - ne * a.nseg_e;
-  if (i < inner * a.nseg_b) {
-    const int sg = i / inner;
-    wx = nl + (i - sg * inner);
-    oy0 = a.y0 + sg * a.seg_b;
-    oy1 = min(oy0 + a.seg_b, a.y1);
-    return;
-  }
-  i -= inner * a.nseg_b;
-  const int sg = i / inner;
-  wx = nl + (i - sg * inner);
-  oy0 = a.y0 + a.nseg_b * a.seg_b + sg * a.seg_s;
-  oy1 = min(oy0 + a.seg_s, a.y1);
+  k1_seg_decode(K1SegPlan{a.seg_e, a.nseg_e, a.seg_b, a.nseg_b, a.seg_s, a.nseg_s}, item, units, nl, nr, a.y0, a.y1,
+                wx, oy0, oy1);
 }
 
 }  // namespace so2dr_dev

@@ -316,6 +316,8 @@ __global__ void __launch_bounds__(NT, 1) k1_stencil3d(const K1Args3D<T> a) {
     __syncthreads();
     const int item = s_item;
     if (item >= total) break;
+    // (the k1_seg_decode order with no edge units, written out: the shared
+    // helper costs this kernel an 8-byte stack frame at its 128-register cap)
     int tz = item / tiles;
     const int rem = item - tz * tiles;
     const int ty = rem / a.nx, tx = rem - ty * a.nx;

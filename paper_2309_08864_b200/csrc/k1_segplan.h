@@ -8,11 +8,53 @@
 #include <mutex>
 #include <tuple>
 
+#if defined(__CUDACC__)
+#define SO2DR_HD __host__ __device__ __forceinline__
+#else
+#define SO2DR_HD inline
+#endif
+
 namespace so2dr_dev {
 
 struct K1SegPlan {
   int seg_e, nseg_e, seg_b, nseg_b, seg_s, nseg_s;
 };
+
+// Items of a launch: `edge` units (ring-column strips) x nseg_e uniform
+// segments, then the inner units' nseg_b big and nseg_s small segments.
+SO2DR_HD int k1_seg_items(const K1SegPlan& p, int units, int edge) {
+  return edge * p.nseg_e + (units - edge) * (p.nseg_b + p.nseg_s);
+}
+
+// Item -> (unit wx, output rows [oy0, oy1)) in hand-out order: edge units
+// first (nl leading, nr trailing), then the inner units' big segments, then
+// their small segments (segment-major, so consecutive items share rows).
+SO2DR_HD void k1_seg_decode(const K1SegPlan& p, int item, int units, int nl, int nr, int y0, int y1, int& wx,
+                            int& oy0, int& oy1) {
+  const int ne = nl + nr;
+  if (item < ne * p.nseg_e) {
+    const int sg = item / ne;
+    const int j = item - sg * ne;
+    wx = j < nl ? j : units - ne + j;
+    oy0 = y0 + sg * p.seg_e;
+    oy1 = oy0 + p.seg_e < y1 ? oy0 + p.seg_e : y1;
+    return;
+  }
+  const int inner = units - ne;
+  int i = item - ne * p.nseg_e;
+  if (i < inner * p.nseg_b) {
+    const int sg = i / inner;
+    wx = nl + (i - sg * inner);
+    oy0 = y0 + sg * p.seg_b;
+    oy1 = oy0 + p.seg_b < y1 ? oy0 + p.seg_b : y1;
+    return;
+  }
+  i -= inner * p.nseg_b;
+  const int sg = i / inner;
+  wx = nl + (i - sg * inner);
+  oy0 = y0 + p.nseg_b * p.seg_b + sg * p.seg_s;
+  oy1 = oy0 + p.seg_s < y1 ? oy0 + p.seg_s : y1;
+}
 
 // Greedy list-scheduling makespan of the launch's item sequence: `workers`
 // identical workers (resident warps or CTAs) each take the next item when
@@ -88,6 +130,7 @@ inline K1SegPlan k1_plan_segments(int height, int units, int edge_units, int64_t
     const double t = sim.makespan();
     if (t < best_t * (1.0 - 1e-9)) best_t = t, best = p;
   };
+  eval(max_seg, max_seg, 0);  // the uniform plan itself: the guided one is never modelled slower
   for (double fs = min_seg; fs <= max_seg * 1.0001; fs *= 1.25) {
     const int seg_s = std::min(max_seg, (int)fs);
     for (int m = 1; m <= 8; ++m) {

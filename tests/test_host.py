@@ -296,3 +296,19 @@ def test_pci_numa_node_sysfs_lookup(tmp_path):
     assert so2dr.pci_numa_node("0000:41:00.0", str(tmp_path)) == -1
     (d / "numa_node").write_text("-1\n")
     assert so2dr.pci_numa_node("0000:40:00.0", str(tmp_path)) == -1
+
+
+def test_k1_segment_plan(tmp_path):
+    """The K1 launch segmentation (csrc/k1_segplan.h, used by the 2D and 3D
+    launchers and decoded by the kernels with the same k1_seg_decode): built
+    with g++ and checked over 648 launch shapes -- every (strip, output row)
+    covered exactly once, ring-column strips first and small segments last,
+    segments within the cap, never modelled slower than uniform segments."""
+    import subprocess
+
+    exe = tmp_path / "segplan_test"
+    subprocess.run(["g++", "-O2", "-std=c++20", "-I", os.path.join(ROOT, "paper_2309_08864_b200", "csrc"),
+                    os.path.join(ROOT, "tests", "cxx", "segplan_test.cpp"), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout[-2000:]
+    assert "0 failures" in out.stdout

@@ -105,6 +105,13 @@ for s in $steps; do
       SZ3=768 STENCILS=star3d1r,box3d1r KS=1,2,4 timeout 900 python tools/k1_bench.py > $OUT/k3d.log 2>&1
       echo "k3d rc=$?" >> $OUT/summary.txt; cat $OUT/k3d.log >> $OUT/summary.txt
       timeout 900 python -m pytest tests/test_gpu_3d_f64.py tests/test_gpu_fullsize.py -x -q > $OUT/pytest_3d.log 2>&1; echo "pytest 3d rc=$?" >> $OUT/summary.txt ;;
+    sanitize)
+      # the sanitize workload bare first (must pass), then under each tool
+      timeout 300 python tools/sanitize_run.py > $OUT/sanitize_plain.log 2>&1; echo "sanitize plain rc=$?" >> $OUT/summary.txt
+      for tool in memcheck racecheck synccheck initcheck; do
+        timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 50 python tools/sanitize_run.py > $OUT/sanitize_$tool.log 2>&1
+        echo "sanitize $tool rc=$?" >> $OUT/summary.txt; tail -3 $OUT/sanitize_$tool.log >> $OUT/summary.txt
+      done ;;
     ncu3d)
       timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_stencil3d -s 1 -c 1 -o $OUT/k1_3d_star_k4 -f \
         python tools/k1_one3d.py 4 768 star > $OUT/k1_3d.log 2>&1; echo "ncu3d rc=$?" >> $OUT/summary.txt ;;
