@@ -109,7 +109,7 @@ for s in $steps; do
       # the sanitize workload bare first (must pass), then under each tool
       timeout 300 python tools/sanitize_run.py > $OUT/sanitize_plain.log 2>&1; echo "sanitize plain rc=$?" >> $OUT/summary.txt
       for tool in memcheck racecheck synccheck initcheck; do
-        timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 50 python tools/sanitize_run.py > $OUT/sanitize_$tool.log 2>&1
+        timeout 600 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 50 python tools/sanitize_run.py > $OUT/sanitize_$tool.log 2>&1
         echo "sanitize $tool rc=$?" >> $OUT/summary.txt; tail -3 $OUT/sanitize_$tool.log >> $OUT/summary.txt
       done ;;
     ncu3d)
