@@ -549,7 +549,8 @@ def main():
                                   "not the BASELINE metric"} if value_res else None),
         "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": e2e_res["h2d"] // args.steps,
                 "d2h_bytes_per_step": e2e_res["d2h"] // args.steps,
-                "wall_s_per_step": e2e_res["wall_s"] / args.steps},
+                "wall_s_per_step": e2e_res["wall_s"] / args.steps,
+                "rank0_device_ms_per_step": [round(t, 2) for t in e2e_res["per_step_ms"]]},
         "roofline": {"bound": "hbm", "kernel": "K1 k1_stencil2d<float,1,%d,box>" % k_on, "achieved": k_gbs,
                      "peak": hbm, "unit": "GB/s", "frac": k_gbs / hbm, "traffic": traffic,
                      "alg_bytes_per_launch": per_launch,
