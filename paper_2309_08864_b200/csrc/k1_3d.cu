@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 
 #include "k1_2d.cuh"  // fma_rn, cp_async helpers
@@ -422,7 +423,11 @@ cudaError_t launch3(const K1Launch& L, cudaStream_t stream) {
   // warm-up planes and the S(R+1)-plane pipeline fill
   const int ov = H + S * (R + 1) + 4;
   const int min_seg_u = std::max(16, 4 * (H + S * (R + 1)));  // r02-mid: ~8 items per SM
-  int nz_u = std::max(1, (8 * sms + nx * ny - 1) / (nx * ny));
+  static const int ips = [] {  // uniform z items per SM (SO2DR_K3D_IPS: experiments)
+    const char* e = std::getenv("SO2DR_K3D_IPS");
+    return e ? std::max(1, std::atoi(e)) : 8;
+  }();
+  int nz_u = std::max(1, (ips * sms + nx * ny - 1) / (nx * ny));
   nz_u = std::min(nz_u, std::max(1, depth / min_seg_u));
   const int seg_u = std::max(1, (depth + nz_u - 1) / nz_u);
   const K1SegPlan sp = k1_plan_segments(depth, nx * ny, 0, (int64_t)sms * occ, ov, 1.0, std::max(8, 2 * ov), seg_u);
